@@ -1,0 +1,152 @@
+/* solidfmm_b200 — C ABI of the B200-native batched M2M / M2L / L2L translation
+ * library (drop-in for the hot path of the reference library `mpole`).
+ *
+ * Every entry point names the reference interface it replaces; paths are
+ * relative to /root/reference/proj/core. Plain pointers and sizes only; no C++
+ * or torch types cross this boundary. All functions return an sfmm_status and
+ * never throw. Coefficient arithmetic is bit-identical to the reference built
+ * with FMA contraction.
+ *
+ * Coefficient layouts
+ *   AoS  (reference layout, include/mpole/solid.hpp:59-70): one solid is
+ *        P(P+1) reals, row n at n(n+1), (re, im) interleaved over m = 0..n.
+ *        A batch is [n][P(P+1)], contiguous.
+ *   SoA  (device layout, "batch-major"): element c of solid b lives at
+ *        base[c * stride + b], c being the AoS index above and stride >= n the
+ *        batch stride in elements. The planes of Im(C_n^0) are ignored on input
+ *        and written as zeros on output.
+ *   Shifts are [n][3] = (x, y, z), source centre -> target centre
+ *        (include/mpole/pipeline.hpp:11-21).
+ */
+#ifndef SOLIDFMM_B200_H
+#define SOLIDFMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sfmm_status {
+    SFMM_OK = 0,
+    SFMM_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    SFMM_DOMAIN_ERROR = 2,     /* std::domain_error (zero shift)         */
+    SFMM_CUDA_ERROR = 3,       /* no counterpart: device/runtime failure */
+    SFMM_OUT_OF_MEMORY = 4
+} sfmm_status;
+
+typedef enum sfmm_kind { SFMM_M2L = 0, SFMM_M2M = 1, SFMM_L2L = 2 } sfmm_kind;
+typedef enum sfmm_precision { SFMM_F64 = 0, SFMM_F32 = 1 } sfmm_precision;
+
+/* Opaque handle: device copies of the swap-matrix streams and faculty tables
+ * for orders <= `order`, plus library-owned device scratch.
+ * Replaces mpole::operator_data<Real> (operators.hpp:57-95) and, because the
+ * scratch travels with the call, mpole::workspace<Real> (workspace.hpp:18-51). */
+typedef struct sfmm_handle sfmm_handle;
+
+/* operator_data<Real>::operator_data(order, cfg) / acquire() (operators.cpp:123-187).
+ * INVALID_ARGUMENT for order < 1 or order > sfmm_max_order(precision)
+ * (operators.cpp:127-132). mu/nu are the reference's CPU blocking parameters:
+ * validated like kernels.cpp:19-26 when non-zero, otherwise ignored. */
+sfmm_status sfmm_create(sfmm_precision precision, int order, int device,
+                        int mu, int nu, sfmm_handle** out);
+void sfmm_destroy(sfmm_handle* h);
+
+/* operator_data::order() and ::max_order() (86 double / 18 single). */
+int sfmm_order(const sfmm_handle* h);
+int sfmm_max_order(sfmm_precision precision);
+int sfmm_device(const sfmm_handle* h);
+const char* sfmm_status_string(sfmm_status s);
+const char* sfmm_last_error(void); /* thread-local detail for the last failure */
+
+/* Table access, for verification against operator_data::swaps(n).f_dense /
+ * g_dense, faculties() and inv_faculties() (operators.hpp:67-80). f and g
+ * receive (n+1)^2 doubles row-major [m][l]; fac 2P-1 and inv P values in the
+ * handle's precision (as doubles). Any pointer may be NULL. */
+sfmm_status sfmm_get_swap_tables(const sfmm_handle* h, int n, double* f, double* g);
+sfmm_status sfmm_get_faculties(const sfmm_handle* h, double* fac, double* inv);
+
+/* ---- batched translation, host buffers, reference AoS layout -------------
+ * Replaces m2l/m2m/l2l(ops, span<translation_request>, ws) (pipeline.hpp:30-45,
+ * pipeline.cpp:275-369) for one uniform (p_in, p_out) group: validates every
+ * request first (orders >= 1, max(p_in,p_out) <= order -> INVALID_ARGUMENT;
+ * |shift| < min normal -> DOMAIN_ERROR; pipeline.cpp:282-298), and only then
+ * copies in, runs on the device, and overwrites `out`. n == 0 is a no-op.
+ * `out` may alias `in` when p_in == p_out (in-place, pipeline.hpp:11-14). */
+sfmm_status sfmm_translate_host(sfmm_handle* h, sfmm_kind kind, int64_t n,
+                                int p_in, int p_out, const void* in_aos,
+                                const void* shifts, void* out_aos);
+
+/* Mixed orders in one call (the grouping of pipeline.cpp:302-342 happens
+ * inside): request i reads in + in_offset[i] (P_in[i](P_in[i]+1) reals) and
+ * overwrites out + out_offset[i] (P_out[i](P_out[i]+1) reals); offsets are in
+ * elements. Validation as above, all before any output is touched. */
+sfmm_status sfmm_translate_host_mixed(sfmm_handle* h, sfmm_kind kind, int64_t n,
+                                      const int* p_in, const int* p_out,
+                                      const void* in, const int64_t* in_offset,
+                                      const void* shifts, void* out,
+                                      const int64_t* out_offset);
+
+/* ---- batched translation, device buffers, SoA layout ---------------------
+ * The resident-data form of the same call: all pointers are device pointers on
+ * sfmm_device(h). Work is enqueued on `stream` (a cudaStream_t, NULL = default
+ * stream). The zero-shift scan runs on the device ahead of the translation
+ * kernel, which does not write anything when the scan fails; with
+ * SFMM_SYNC_STATUS (default) the call waits for the scan result and returns
+ * DOMAIN_ERROR, with SFMM_ASYNC_STATUS it returns at once and the outcome is
+ * read later with sfmm_stream_status(). */
+enum { SFMM_SYNC_STATUS = 0, SFMM_ASYNC_STATUS = 1 };
+sfmm_status sfmm_translate_soa(sfmm_handle* h, sfmm_kind kind, int64_t n,
+                               int p_in, int p_out, const void* d_in,
+                               int64_t in_stride, const void* d_shifts,
+                               void* d_out, int64_t out_stride, void* stream,
+                               int flags);
+/* Synchronises `stream` and reports the status of the SoA calls enqueued with
+ * SFMM_ASYNC_STATUS since the last query (DOMAIN_ERROR if any scan failed). */
+sfmm_status sfmm_stream_status(sfmm_handle* h, void* stream);
+
+/* AoS <-> SoA repacking on the device (batch of n solids of order p). */
+sfmm_status sfmm_pack_soa(sfmm_handle* h, int64_t n, int p, const void* d_aos,
+                          void* d_soa, int64_t stride, void* stream);
+sfmm_status sfmm_unpack_soa(sfmm_handle* h, int64_t n, int p, const void* d_soa,
+                            int64_t stride, void* d_aos, void* stream);
+
+/* ---- target-owned M2L accumulation (a full interaction-list level) -------
+ * L[t] = sum over the sources s of target t of m2l(M[s], shift(t, s)), each
+ * term computed exactly as the batched call computes it, summed without
+ * atomics in a fixed order. The reference has
+ * no such entry point (it overwrites: pipeline.cpp:258-265); a caller of the
+ * reference issues one request per pair and adds the outputs itself.
+ *
+ * The plan holds the pair list in CSR form over targets: pairs
+ * tgt_ptr[t] .. tgt_ptr[t+1]-1 belong to target t; pair j reads source
+ * src_index[j] with shift shifts[3j..3j+2]. All plan inputs are HOST pointers
+ * and are validated (zero shifts -> DOMAIN_ERROR) when the plan is built. */
+typedef struct sfmm_plan sfmm_plan;
+sfmm_status sfmm_plan_create(sfmm_handle* h, int64_t n_targets,
+                             const int64_t* tgt_ptr, const int32_t* src_index,
+                             const void* shifts, int64_t n_sources,
+                             sfmm_plan** out);
+void sfmm_plan_destroy(sfmm_plan* plan);
+int64_t sfmm_plan_pairs(const sfmm_plan* plan);
+
+/* Device SoA sources [c][src_stride], device SoA outputs [c][out_stride]
+ * (overwritten with the sums; targets without pairs receive zeros). */
+sfmm_status sfmm_m2l_accumulate(sfmm_handle* h, const sfmm_plan* plan, int p_in,
+                                int p_out, const void* d_src, int64_t src_stride,
+                                void* d_out, int64_t out_stride, void* stream);
+
+/* Host AoS form of the same: sources [n_sources][P_in(P_in+1)], outputs
+ * [n_targets][P_out(P_out+1)], copies inside the call. */
+sfmm_status sfmm_m2l_accumulate_host(sfmm_handle* h, const sfmm_plan* plan,
+                                     int p_in, int p_out, const void* src_aos,
+                                     void* out_aos);
+
+/* Number of kernel launches this handle has issued (bench.py gpu_launches). */
+int64_t sfmm_launch_count(const sfmm_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOLIDFMM_B200_H */

@@ -1,0 +1,270 @@
+"""ctypes binding of the C ABI declared in include/solidfmm_b200.h.
+
+This is the only way Python reaches the CUDA library; there is no CPU
+fallback. Importing the module does not need a GPU (the shared library loads
+and exports its symbols on any host), creating a handle does.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_void_p
+from pathlib import Path
+
+import numpy as np
+
+from . import build as _build
+
+OK, INVALID_ARGUMENT, DOMAIN_ERROR, CUDA_ERROR, OUT_OF_MEMORY = range(5)
+M2L, M2M, L2L = 0, 1, 2
+F64, F32 = 0, 1
+SYNC_STATUS, ASYNC_STATUS = 0, 1
+
+KIND_BY_NAME = {"m2l": M2L, "m2m": M2M, "l2l": L2L}
+
+# every symbol include/solidfmm_b200.h declares: (restype, argtypes)
+_SIGNATURES = {
+    "sfmm_create": (c_int, [c_int, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
+    "sfmm_destroy": (None, [c_void_p]),
+    "sfmm_order": (c_int, [c_void_p]),
+    "sfmm_max_order": (c_int, [c_int]),
+    "sfmm_device": (c_int, [c_void_p]),
+    "sfmm_status_string": (c_char_p, [c_int]),
+    "sfmm_last_error": (c_char_p, []),
+    "sfmm_get_swap_tables": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "sfmm_get_faculties": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "sfmm_translate_host": (c_int, [c_void_p, c_int, c_int64, c_int, c_int, c_void_p, c_void_p,
+                                    c_void_p]),
+    "sfmm_translate_host_mixed": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sfmm_translate_soa": (c_int, [c_void_p, c_int, c_int64, c_int, c_int, c_void_p, c_int64,
+                                   c_void_p, c_void_p, c_int64, c_void_p, c_int]),
+    "sfmm_stream_status": (c_int, [c_void_p, c_void_p]),
+    "sfmm_pack_soa": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int64, c_void_p]),
+    "sfmm_unpack_soa": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_int64, c_void_p, c_void_p]),
+    "sfmm_plan_create": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
+                                 POINTER(c_void_p)]),
+    "sfmm_plan_destroy": (None, [c_void_p]),
+    "sfmm_plan_pairs": (c_int64, [c_void_p]),
+    "sfmm_m2l_accumulate": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_int64, c_void_p,
+                                    c_int64, c_void_p]),
+    "sfmm_m2l_accumulate_host": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "sfmm_launch_count": (c_int64, [c_void_p]),
+}
+
+_lib = None
+
+
+def library_path() -> Path:
+    return _build.LIB_PATH
+
+
+def load_library() -> ctypes.CDLL:
+    """Load libsolidfmm_b200.so; raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        path = library_path()
+        if not path.exists():
+            raise RuntimeError(
+                f"{path} is missing: build it with `python -m paper_2202_02847_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(str(path))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)  # AttributeError = header/library mismatch
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class SfmmError(Exception):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{status_name(status)}: {detail}")
+        self.status = status
+        self.detail = detail
+
+
+class InvalidArgument(SfmmError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class DomainError(SfmmError, ArithmeticError):
+    """std::domain_error in the reference (zero shift vector)."""
+
+
+def status_name(status: int) -> str:
+    return load_library().sfmm_status_string(status).decode()
+
+
+def check(status: int) -> None:
+    if status == OK:
+        return
+    detail = load_library().sfmm_last_error().decode()
+    if status == INVALID_ARGUMENT:
+        raise InvalidArgument(status, detail)
+    if status == DOMAIN_ERROR:
+        raise DomainError(status, detail)
+    raise SfmmError(status, detail)
+
+
+def max_order(precision: int) -> int:
+    return load_library().sfmm_max_order(precision)
+
+
+def dtype_of(precision: int):
+    return np.float64 if precision == F64 else np.float32
+
+
+def solid_size(order: int) -> int:
+    return order * (order + 1)
+
+
+def _ptr(a) -> c_void_p:
+    """Host numpy array, raw address (int) or None -> void*."""
+    if a is None:
+        return c_void_p(None)
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(c_void_p)
+    return c_void_p(int(a))
+
+
+class Handle:
+    """Owns one `sfmm_handle*` (the reference's operator_data + workspace)."""
+
+    def __init__(self, precision: int, order: int, device: int = 0, mu: int = 0, nu: int = 0):
+        self._lib = load_library()
+        self._h = c_void_p(None)
+        self.precision = precision
+        self.dtype = dtype_of(precision)
+        check(self._lib.sfmm_create(precision, order, device, mu, nu, ctypes.byref(self._h)))
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.sfmm_destroy(self._h)
+            self._h = c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def order(self) -> int:
+        return self._lib.sfmm_order(self._h)
+
+    @property
+    def device(self) -> int:
+        return self._lib.sfmm_device(self._h)
+
+    @property
+    def launch_count(self) -> int:
+        return self._lib.sfmm_launch_count(self._h)
+
+    def swap_tables(self, n: int):
+        f = np.empty((n + 1, n + 1), np.float64)
+        g = np.empty((n + 1, n + 1), np.float64)
+        check(self._lib.sfmm_get_swap_tables(self._h, n, _ptr(f), _ptr(g)))
+        return f, g
+
+    def faculties(self):
+        p = self.order
+        fac = np.empty(2 * p - 1, np.float64)
+        inv = np.empty(p, np.float64)
+        check(self._lib.sfmm_get_faculties(self._h, _ptr(fac), _ptr(inv)))
+        return fac, inv
+
+    # -- host AoS ---------------------------------------------------------
+    def translate_host(self, kind: int, p_in: int, p_out: int, src: np.ndarray,
+                       shifts: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        src = np.ascontiguousarray(src, self.dtype)
+        shifts = np.ascontiguousarray(shifts, self.dtype)
+        n = shifts.shape[0] if shifts.ndim == 2 else shifts.size // 3
+        if out is None:
+            out = np.empty((n, solid_size(max(p_out, 1))), self.dtype)
+        check(self._lib.sfmm_translate_host(self._h, kind, n, p_in, p_out, _ptr(src),
+                                            _ptr(shifts), _ptr(out)))
+        return out
+
+    def translate_host_mixed(self, kind: int, p_in, p_out, src: np.ndarray, in_off, shifts,
+                             out: np.ndarray, out_off) -> np.ndarray:
+        p_in = np.ascontiguousarray(p_in, np.int32)
+        p_out = np.ascontiguousarray(p_out, np.int32)
+        in_off = np.ascontiguousarray(in_off, np.int64)
+        out_off = np.ascontiguousarray(out_off, np.int64)
+        shifts = np.ascontiguousarray(shifts, self.dtype)
+        check(self._lib.sfmm_translate_host_mixed(self._h, kind, len(p_in), _ptr(p_in),
+                                                  _ptr(p_out), _ptr(src), _ptr(in_off),
+                                                  _ptr(shifts), _ptr(out), _ptr(out_off)))
+        return out
+
+    # -- device SoA (raw device addresses, e.g. torch.Tensor.data_ptr()) --
+    def translate_soa(self, kind: int, n: int, p_in: int, p_out: int, d_in, in_stride: int,
+                      d_shifts, d_out, out_stride: int, stream=None, flags: int = SYNC_STATUS):
+        check(self._lib.sfmm_translate_soa(self._h, kind, n, p_in, p_out, _ptr(d_in), in_stride,
+                                           _ptr(d_shifts), _ptr(d_out), out_stride, _ptr(stream),
+                                           flags))
+
+    def stream_status(self, stream=None) -> None:
+        check(self._lib.sfmm_stream_status(self._h, _ptr(stream)))
+
+    def pack_soa(self, n: int, p: int, d_aos, d_soa, stride: int, stream=None) -> None:
+        check(self._lib.sfmm_pack_soa(self._h, n, p, _ptr(d_aos), _ptr(d_soa), stride,
+                                      _ptr(stream)))
+
+    def unpack_soa(self, n: int, p: int, d_soa, stride: int, d_aos, stream=None) -> None:
+        check(self._lib.sfmm_unpack_soa(self._h, n, p, _ptr(d_soa), stride, _ptr(d_aos),
+                                        _ptr(stream)))
+
+    # -- target-owned accumulation -----------------------------------------
+    def plan(self, tgt_ptr, src_index, shifts, n_sources: int) -> "Plan":
+        return Plan(self, tgt_ptr, src_index, shifts, n_sources)
+
+
+class Plan:
+    def __init__(self, handle: Handle, tgt_ptr, src_index, shifts, n_sources: int):
+        self._handle = handle
+        self._lib = handle._lib
+        tgt_ptr = np.ascontiguousarray(tgt_ptr, np.int64)
+        src_index = np.ascontiguousarray(src_index, np.int32)
+        shifts = np.ascontiguousarray(shifts, handle.dtype)
+        self.n_targets = len(tgt_ptr) - 1
+        self.n_sources = n_sources
+        self._p = c_void_p(None)
+        check(self._lib.sfmm_plan_create(handle._h, self.n_targets, _ptr(tgt_ptr),
+                                         _ptr(src_index), _ptr(shifts), n_sources,
+                                         ctypes.byref(self._p)))
+
+    @property
+    def pairs(self) -> int:
+        return self._lib.sfmm_plan_pairs(self._p)
+
+    def close(self) -> None:
+        if self._p:
+            self._lib.sfmm_plan_destroy(self._p)
+            self._p = c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def accumulate(self, p_in: int, p_out: int, d_src, src_stride: int, d_out, out_stride: int,
+                   stream=None) -> None:
+        check(self._lib.sfmm_m2l_accumulate(self._handle._h, self._p, p_in, p_out, _ptr(d_src),
+                                            src_stride, _ptr(d_out), out_stride, _ptr(stream)))
+
+    def accumulate_host(self, p_in: int, p_out: int, src: np.ndarray,
+                        out: np.ndarray | None = None) -> np.ndarray:
+        src = np.ascontiguousarray(src, self._handle.dtype)
+        if out is None:
+            out = np.empty((self.n_targets, solid_size(p_out)), self._handle.dtype)
+        check(self._lib.sfmm_m2l_accumulate_host(self._handle._h, self._p, p_in, p_out, _ptr(src),
+                                                 _ptr(out)))
+        return out

@@ -1,0 +1,666 @@
+// C-ABI layer: handle management, validation, host <-> device staging.
+// See include/solidfmm_b200.h for the contract of every entry point.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "sfmm_internal.hpp"
+#include "solidfmm_b200.h"
+
+using namespace sfmm;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sfmm_status fail(sfmm_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+sfmm_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(e == cudaErrorMemoryAllocation ? SFMM_OUT_OF_MEMORY : SFMM_CUDA_ERROR,
+                std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CU(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);       \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+constexpr int kFlagSlots = 256;
+
+size_t elem_size(int precision) { return precision == SFMM_F64 ? 8 : 4; }
+int64_t round_up32(int64_t n) { return (n + 31) / 32 * 32; }
+int64_t solid_len(int p) { return (int64_t)p * (p + 1); }
+
+}  // namespace
+
+struct sfmm_handle {
+    int precision = SFMM_F64;
+    int order = 0;
+    int device = 0;
+    int sm_count = 0;
+    SwapTables host_tables{1};
+    std::vector<double> fac, inv;  // values in the handle precision, widened
+    DeviceTables<double> td;
+    DeviceTables<float> tf;
+    std::vector<void*> allocations;
+    int* d_flags = nullptr;
+    int* h_flags = nullptr;  // pinned
+    std::atomic<unsigned> flag_cursor{0};
+    std::atomic<int64_t> launches{0};
+    std::mutex async_mutex;
+    std::vector<int> async_slots;
+};
+
+struct sfmm_plan {
+    sfmm_handle* h = nullptr;
+    int64_t n_targets = 0, n_pairs = 0, n_groups = 0, n_sources = 0;
+    int64_t* d_grp_ptr = nullptr;   // [n_targets + 1]
+    int32_t* d_src_index = nullptr; // [n_groups * 32], -1 = idle lane
+    void* d_shifts = nullptr;       // [n_groups * 32][3]
+};
+
+namespace {
+
+template <typename Real>
+sfmm_status upload_tables(sfmm_handle* h, DeviceTables<Real>& t) {
+    t.order = h->order;
+    for (int side = 0; side < 2; ++side) {
+        const PackedSide ps = pack_side(h->host_tables, side == 1);
+        std::vector<Real> s(ps.stream.size());
+        for (size_t i = 0; i < s.size(); ++i) s[i] = static_cast<Real>(ps.stream[i]);
+        Real* ds = nullptr;
+        BlockDesc* dd = nullptr;
+        CU(cudaMalloc((void**)&ds, std::max<size_t>(s.size(), 2) * sizeof(Real)));
+        h->allocations.push_back(ds);
+        CU(cudaMalloc((void**)&dd, ps.desc.size() * sizeof(BlockDesc)));
+        h->allocations.push_back(dd);
+        CU(cudaMemcpy(ds, s.data(), s.size() * sizeof(Real), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dd, ps.desc.data(), ps.desc.size() * sizeof(BlockDesc),
+                      cudaMemcpyHostToDevice));
+        t.stream[side] = ds;
+        t.desc[side] = dd;
+        t.stream_len[side] = (uint32_t)s.size();
+    }
+    std::vector<Real> fac, inv;
+    build_faculties<Real>(h->order, fac, inv);
+    std::vector<Real> winv(inv);
+    for (size_t d = 1; d < winv.size(); d += 2) winv[d] = -winv[d];
+    h->fac.assign(fac.begin(), fac.end());
+    h->inv.assign(inv.begin(), inv.end());
+    Real *dfac = nullptr, *dinv = nullptr, *dwinv = nullptr;
+    CU(cudaMalloc((void**)&dfac, fac.size() * sizeof(Real)));
+    h->allocations.push_back(dfac);
+    CU(cudaMalloc((void**)&dinv, inv.size() * sizeof(Real)));
+    h->allocations.push_back(dinv);
+    CU(cudaMalloc((void**)&dwinv, winv.size() * sizeof(Real)));
+    h->allocations.push_back(dwinv);
+    CU(cudaMemcpy(dfac, fac.data(), fac.size() * sizeof(Real), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dinv, inv.data(), inv.size() * sizeof(Real), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dwinv, winv.data(), winv.size() * sizeof(Real), cudaMemcpyHostToDevice));
+    t.fac = dfac;
+    t.inv = dinv;
+    t.winv = dwinv;
+    return SFMM_OK;
+}
+
+template <typename Real>
+const DeviceTables<Real>& tables_of(const sfmm_handle* h);
+template <>
+const DeviceTables<double>& tables_of<double>(const sfmm_handle* h) { return h->td; }
+template <>
+const DeviceTables<float>& tables_of<float>(const sfmm_handle* h) { return h->tf; }
+
+sfmm_status check_orders(const sfmm_handle* h, int kind, int p_in, int p_out) {
+    if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
+    if (kind < 0 || kind > 2) return fail(SFMM_INVALID_ARGUMENT, "unknown translation kind");
+    // pipeline.cpp:285-295
+    if (p_in < 1 || p_out < 1)
+        return fail(SFMM_INVALID_ARGUMENT, "translation orders must be >= 1");
+    if (std::max(p_in, p_out) > h->order)
+        return fail(SFMM_INVALID_ARGUMENT, "translation order exceeds operator data order");
+    return SFMM_OK;
+}
+
+// pipeline.cpp:296-297: norm(shift) < numeric_limits<Real>::min()
+template <typename Real>
+bool host_shift_degenerate(const Real* r) {
+    return std::hypot(r[0], r[1], r[2]) < std::numeric_limits<Real>::min();
+}
+
+template <typename Real>
+sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, int p_out,
+                               const Real* d_in, int64_t in_stride, const Real* d_shifts,
+                               Real* d_out, int64_t out_stride, cudaStream_t stream, int flags,
+                               bool skip_scan) {
+    int slot = -1;
+    int* d_flag = nullptr;
+    if (!skip_scan) {
+        slot = (int)(h->flag_cursor.fetch_add(1) % kFlagSlots);
+        d_flag = h->d_flags + slot;
+        CU(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
+        CU(launch_check_shifts<Real>(d_shifts, n, d_flag, stream));
+        h->launches += 1;
+    }
+    TranslateArgs<Real> a;
+    a.kind = kind;
+    a.p_in = p_in;
+    a.p_out = p_out;
+    a.n = n;
+    a.in = d_in;
+    a.in_stride = in_stride;
+    a.shifts = d_shifts;
+    a.out = d_out;
+    a.out_stride = out_stride;
+    a.fail_flag = d_flag;
+    LaunchInfo info;
+    CU(launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info));
+    h->launches += info.launches;
+    if (skip_scan) return SFMM_OK;
+    if (flags & SFMM_ASYNC_STATUS) {
+        std::lock_guard<std::mutex> lk(h->async_mutex);
+        h->async_slots.push_back(slot);
+        return SFMM_OK;
+    }
+    CU(cudaMemcpyAsync(h->h_flags + slot, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CU(cudaStreamSynchronize(stream));
+    if (h->h_flags[slot]) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
+    return SFMM_OK;
+}
+
+template <typename Real>
+sfmm_status translate_host_impl(sfmm_handle* h, int kind, int64_t n, int p_in, int p_out,
+                                const Real* in, const Real* shifts, Real* out) {
+    for (int64_t i = 0; i < n; ++i)
+        if (host_shift_degenerate(shifts + 3 * i))
+            return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
+    const int64_t si = solid_len(p_in), so = solid_len(p_out), stride = round_up32(n);
+    cudaStream_t stream = nullptr;
+    Real *d_in_aos = nullptr, *d_in = nullptr, *d_sh = nullptr, *d_out = nullptr,
+         *d_out_aos = nullptr;
+    const size_t es = sizeof(Real);
+    CU(cudaMallocAsync((void**)&d_in_aos, es * si * n, stream));
+    CU(cudaMallocAsync((void**)&d_in, es * si * stride, stream));
+    CU(cudaMallocAsync((void**)&d_sh, es * 3 * n, stream));
+    CU(cudaMallocAsync((void**)&d_out, es * so * stride, stream));
+    CU(cudaMallocAsync((void**)&d_out_aos, es * so * n, stream));
+    CU(cudaMemcpyAsync(d_in_aos, in, es * si * n, cudaMemcpyHostToDevice, stream));
+    CU(cudaMemcpyAsync(d_sh, shifts, es * 3 * n, cudaMemcpyHostToDevice, stream));
+    CU(launch_pack_soa<Real>(d_in_aos, d_in, n, p_in, stride, stream));
+    sfmm_status st = translate_soa_impl<Real>(h, kind, n, p_in, p_out, d_in, stride, d_sh, d_out,
+                                              stride, stream, 0, /*skip_scan=*/true);
+    if (st == SFMM_OK) {
+        cudaError_t e = launch_unpack_soa<Real>(d_out, d_out_aos, n, p_out, stride, stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out, d_out_aos, es * so * n, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) st = cuda_fail(e, "translate_host");
+        h->launches += 2;
+    }
+    cudaFreeAsync(d_in_aos, stream);
+    cudaFreeAsync(d_in, stream);
+    cudaFreeAsync(d_sh, stream);
+    cudaFreeAsync(d_out, stream);
+    cudaFreeAsync(d_out_aos, stream);
+    return st;
+}
+
+template <typename Real>
+sfmm_status translate_host_mixed_impl(sfmm_handle* h, int kind, int64_t n, const int* p_in,
+                                      const int* p_out, const Real* in, const int64_t* in_off,
+                                      const Real* shifts, Real* out, const int64_t* out_off) {
+    // validate everything first (pipeline.cpp:282-298)
+    for (int64_t i = 0; i < n; ++i) {
+        const sfmm_status st = check_orders(h, kind, p_in[i], p_out[i]);
+        if (st != SFMM_OK) return st;
+        if (host_shift_degenerate(shifts + 3 * i))
+            return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
+    }
+    // group by order pair, keeping the request order inside a group (pipeline.cpp:302-308)
+    std::vector<int64_t> idx(n);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+        if (p_in[a] != p_in[b]) return p_in[a] < p_in[b];
+        return p_out[a] < p_out[b];
+    });
+    // sources are staged before any output is written, so an output may alias
+    // its own source even when the order changes (pipeline.cpp:312-324)
+    std::vector<std::vector<Real>> stage_in, stage_sh;
+    std::vector<std::pair<int64_t, int64_t>> ranges;
+    for (int64_t i = 0; i < n;) {
+        int64_t j = i;
+        while (j < n && p_in[idx[j]] == p_in[idx[i]] && p_out[idx[j]] == p_out[idx[i]]) ++j;
+        const int64_t si = solid_len(p_in[idx[i]]);
+        std::vector<Real> gi((size_t)(si * (j - i))), gs((size_t)(3 * (j - i)));
+        for (int64_t k = i; k < j; ++k) {
+            std::memcpy(&gi[(size_t)((k - i) * si)], in + in_off[idx[k]], sizeof(Real) * si);
+            std::memcpy(&gs[(size_t)(3 * (k - i))], shifts + 3 * idx[k], sizeof(Real) * 3);
+        }
+        stage_in.push_back(std::move(gi));
+        stage_sh.push_back(std::move(gs));
+        ranges.emplace_back(i, j);
+        i = j;
+    }
+    for (size_t g = 0; g < ranges.size(); ++g) {
+        const int64_t i = ranges[g].first, j = ranges[g].second;
+        const int pi = p_in[idx[i]], po = p_out[idx[i]];
+        const int64_t so = solid_len(po);
+        std::vector<Real> go((size_t)(so * (j - i)));
+        const sfmm_status st = translate_host_impl<Real>(h, kind, j - i, pi, po, stage_in[g].data(),
+                                                         stage_sh[g].data(), go.data());
+        if (st != SFMM_OK) return st;
+        for (int64_t k = i; k < j; ++k)
+            std::memcpy(out + out_off[idx[k]], &go[(size_t)((k - i) * so)], sizeof(Real) * so);
+    }
+    return SFMM_OK;
+}
+
+template <typename Real>
+sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tgt_ptr,
+                             const int32_t* src_index, const Real* shifts, int64_t n_sources,
+                             sfmm_plan* plan) {
+    const int64_t n_pairs = tgt_ptr[n_targets];
+    std::vector<int64_t> grp_ptr((size_t)n_targets + 1, 0);
+    for (int64_t t = 0; t < n_targets; ++t) {
+        const int64_t cnt = tgt_ptr[t + 1] - tgt_ptr[t];
+        if (cnt < 0) return fail(SFMM_INVALID_ARGUMENT, "tgt_ptr must be non-decreasing");
+        grp_ptr[(size_t)t + 1] = grp_ptr[(size_t)t] + (cnt + 31) / 32;
+    }
+    const int64_t n_groups = grp_ptr[(size_t)n_targets];
+    std::vector<int32_t> si((size_t)n_groups * 32, -1);
+    std::vector<Real> sh((size_t)n_groups * 32 * 3);
+    for (size_t i = 0; i < (size_t)n_groups * 32; ++i) {
+        sh[3 * i] = 0;
+        sh[3 * i + 1] = 0;
+        sh[3 * i + 2] = 1;
+    }
+    for (int64_t t = 0; t < n_targets; ++t) {
+        int64_t dst = grp_ptr[(size_t)t] * 32;
+        for (int64_t j = tgt_ptr[t]; j < tgt_ptr[t + 1]; ++j, ++dst) {
+            if (src_index[j] < 0 || src_index[j] >= n_sources)
+                return fail(SFMM_INVALID_ARGUMENT, "source index out of range");
+            if (host_shift_degenerate(shifts + 3 * j))
+                return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
+            si[(size_t)dst] = src_index[j];
+            std::memcpy(&sh[(size_t)(3 * dst)], shifts + 3 * j, sizeof(Real) * 3);
+        }
+    }
+    plan->h = h;
+    plan->n_targets = n_targets;
+    plan->n_pairs = n_pairs;
+    plan->n_groups = n_groups;
+    plan->n_sources = n_sources;
+    CU(cudaMalloc((void**)&plan->d_grp_ptr, sizeof(int64_t) * grp_ptr.size()));
+    CU(cudaMalloc((void**)&plan->d_src_index, sizeof(int32_t) * std::max<size_t>(si.size(), 1)));
+    CU(cudaMalloc(&plan->d_shifts, sizeof(Real) * std::max<size_t>(sh.size(), 1)));
+    CU(cudaMemcpy(plan->d_grp_ptr, grp_ptr.data(), sizeof(int64_t) * grp_ptr.size(),
+                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(plan->d_src_index, si.data(), sizeof(int32_t) * si.size(),
+                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(plan->d_shifts, sh.data(), sizeof(Real) * sh.size(), cudaMemcpyHostToDevice));
+    return SFMM_OK;
+}
+
+template <typename Real>
+sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,
+                            const Real* d_src, int64_t src_stride, Real* d_out,
+                            int64_t out_stride, cudaStream_t stream) {
+    const int64_t so = solid_len(p_out);
+    Real* partial = nullptr;
+    if (plan->n_groups > 0)
+        CU(cudaMallocAsync((void**)&partial, sizeof(Real) * so * plan->n_groups, stream));
+    TranslateArgs<Real> a;
+    a.kind = KIND_M2L;
+    a.p_in = p_in;
+    a.p_out = p_out;
+    a.n = plan->n_groups * 32;
+    a.in = d_src;
+    a.in_stride = src_stride;
+    a.shifts = static_cast<const Real*>(plan->d_shifts);
+    a.out = partial;
+    a.out_stride = plan->n_groups;
+    a.src_index = plan->d_src_index;
+    LaunchInfo info;
+    cudaError_t e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
+    h->launches += info.launches;
+    if (e == cudaSuccess) {
+        e = launch_reduce_groups<Real>(partial, plan->n_groups, plan->d_grp_ptr, plan->n_targets,
+                                       p_out, d_out, out_stride, stream);
+        h->launches += 1;
+    }
+    if (partial) cudaFreeAsync(partial, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "m2l_accumulate");
+    return SFMM_OK;
+}
+
+template <typename Real>
+sfmm_status accumulate_host_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,
+                                 const Real* src_aos, Real* out_aos) {
+    const int64_t si = solid_len(p_in), so = solid_len(p_out);
+    const int64_t ns = plan->n_sources, nt = plan->n_targets;
+    const int64_t sstride = round_up32(ns), ostride = round_up32(nt);
+    cudaStream_t stream = nullptr;
+    const size_t es = sizeof(Real);
+    Real *d_src_aos = nullptr, *d_src = nullptr, *d_out = nullptr, *d_out_aos = nullptr;
+    CU(cudaMallocAsync((void**)&d_src_aos, es * si * ns, stream));
+    CU(cudaMallocAsync((void**)&d_src, es * si * sstride, stream));
+    CU(cudaMallocAsync((void**)&d_out, es * so * ostride, stream));
+    CU(cudaMallocAsync((void**)&d_out_aos, es * so * nt, stream));
+    CU(cudaMemcpyAsync(d_src_aos, src_aos, es * si * ns, cudaMemcpyHostToDevice, stream));
+    CU(launch_pack_soa<Real>(d_src_aos, d_src, ns, p_in, sstride, stream));
+    sfmm_status st =
+        accumulate_impl<Real>(h, plan, p_in, p_out, d_src, sstride, d_out, ostride, stream);
+    if (st == SFMM_OK) {
+        cudaError_t e = launch_unpack_soa<Real>(d_out, d_out_aos, nt, p_out, ostride, stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out_aos, d_out_aos, es * so * nt, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) st = cuda_fail(e, "m2l_accumulate_host");
+        h->launches += 2;
+    }
+    cudaFreeAsync(d_src_aos, stream);
+    cudaFreeAsync(d_src, stream);
+    cudaFreeAsync(d_out, stream);
+    cudaFreeAsync(d_out_aos, stream);
+    return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sfmm_status_string(sfmm_status s) {
+    switch (s) {
+        case SFMM_OK: return "ok";
+        case SFMM_INVALID_ARGUMENT: return "invalid argument";
+        case SFMM_DOMAIN_ERROR: return "domain error";
+        case SFMM_CUDA_ERROR: return "CUDA error";
+        case SFMM_OUT_OF_MEMORY: return "out of device memory";
+    }
+    return "unknown status";
+}
+
+const char* sfmm_last_error(void) { return g_last_error.c_str(); }
+
+int sfmm_max_order(sfmm_precision precision) {
+    return precision == SFMM_F32 ? max_order_f32() : max_order_f64();
+}
+
+sfmm_status sfmm_create(sfmm_precision precision, int order, int device, int mu, int nu,
+                        sfmm_handle** out) {
+    if (!out) return fail(SFMM_INVALID_ARGUMENT, "null output pointer");
+    *out = nullptr;
+    if (precision != SFMM_F64 && precision != SFMM_F32)
+        return fail(SFMM_INVALID_ARGUMENT, "unknown precision");
+    // kernels.cpp:19-26 (only when the caller passes a config)
+    if (mu != 0 && (mu < 2 || (mu & 1) || mu > 32))
+        return fail(SFMM_INVALID_ARGUMENT, "kernel_config: mu must be even, 2 <= mu <= 32");
+    if (nu != 0 && (nu < 1 || nu > 64))
+        return fail(SFMM_INVALID_ARGUMENT, "kernel_config: nu must satisfy 1 <= nu <= 64");
+    // operators.cpp:127-132
+    if (order < 1) return fail(SFMM_INVALID_ARGUMENT, "order must be >= 1");
+    if (order > sfmm_max_order(precision))
+        return fail(SFMM_INVALID_ARGUMENT,
+                    "order too large: faculty table overflows (cap " +
+                        std::to_string(sfmm_max_order(precision)) + ")");
+    int count = 0;
+    CU(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail(SFMM_INVALID_ARGUMENT, "no such CUDA device");
+    DeviceGuard guard(device);
+    if (!guard.ok) return fail(SFMM_CUDA_ERROR, "cudaSetDevice failed");
+
+    auto* h = new sfmm_handle;
+    h->precision = precision;
+    h->order = order;
+    h->device = device;
+    h->host_tables = SwapTables(order);
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e, "cudaGetDeviceProperties");
+    }
+    h->sm_count = prop.multiProcessorCount;
+    sfmm_status st = precision == SFMM_F64 ? upload_tables<double>(h, h->td)
+                                           : upload_tables<float>(h, h->tf);
+    if (st == SFMM_OK) {
+        if (cudaMalloc((void**)&h->d_flags, sizeof(int) * kFlagSlots) != cudaSuccess ||
+            cudaMemset(h->d_flags, 0, sizeof(int) * kFlagSlots) != cudaSuccess ||
+            cudaMallocHost((void**)&h->h_flags, sizeof(int) * kFlagSlots) != cudaSuccess)
+            st = fail(SFMM_CUDA_ERROR, "status flag allocation failed");
+    }
+    if (st != SFMM_OK) {
+        sfmm_destroy(h);
+        return st;
+    }
+    *out = h;
+    return SFMM_OK;
+}
+
+void sfmm_destroy(sfmm_handle* h) {
+    if (!h) return;
+    DeviceGuard guard(h->device);
+    for (void* p : h->allocations) cudaFree(p);
+    if (h->d_flags) cudaFree(h->d_flags);
+    if (h->h_flags) cudaFreeHost(h->h_flags);
+    delete h;
+}
+
+int sfmm_order(const sfmm_handle* h) { return h ? h->order : 0; }
+int sfmm_device(const sfmm_handle* h) { return h ? h->device : -1; }
+int64_t sfmm_launch_count(const sfmm_handle* h) { return h ? h->launches.load() : 0; }
+
+sfmm_status sfmm_get_swap_tables(const sfmm_handle* h, int n, double* f, double* g) {
+    if (!h || n < 0 || n >= h->order) return fail(SFMM_INVALID_ARGUMENT, "row out of range");
+    const size_t sz = (size_t)(n + 1) * (n + 1);
+    const bool single = h->precision == SFMM_F32;
+    for (size_t i = 0; i < sz; ++i) {
+        // operators.cpp:152-155: the library precision sees the double tables cast
+        if (f) f[i] = single ? (double)(float)h->host_tables.f[n][i] : h->host_tables.f[n][i];
+        if (g) g[i] = single ? (double)(float)h->host_tables.g[n][i] : h->host_tables.g[n][i];
+    }
+    return SFMM_OK;
+}
+
+sfmm_status sfmm_get_faculties(const sfmm_handle* h, double* fac, double* inv) {
+    if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
+    if (fac) std::copy(h->fac.begin(), h->fac.end(), fac);
+    if (inv) std::copy(h->inv.begin(), h->inv.end(), inv);
+    return SFMM_OK;
+}
+
+sfmm_status sfmm_translate_host(sfmm_handle* h, sfmm_kind kind, int64_t n, int p_in, int p_out,
+                                const void* in_aos, const void* shifts, void* out_aos) {
+    if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
+    if (n < 0) return fail(SFMM_INVALID_ARGUMENT, "negative batch size");
+    if (n == 0) return SFMM_OK;  // pipeline.cpp:280
+    if (!in_aos || !shifts || !out_aos)
+        return fail(SFMM_INVALID_ARGUMENT, "translation request with null solid");
+    const sfmm_status st = check_orders(h, kind, p_in, p_out);
+    if (st != SFMM_OK) return st;
+    DeviceGuard guard(h->device);
+    if (h->precision == SFMM_F64)
+        return translate_host_impl<double>(h, kind, n, p_in, p_out, (const double*)in_aos,
+                                           (const double*)shifts, (double*)out_aos);
+    return translate_host_impl<float>(h, kind, n, p_in, p_out, (const float*)in_aos,
+                                      (const float*)shifts, (float*)out_aos);
+}
+
+sfmm_status sfmm_translate_host_mixed(sfmm_handle* h, sfmm_kind kind, int64_t n, const int* p_in,
+                                      const int* p_out, const void* in, const int64_t* in_offset,
+                                      const void* shifts, void* out, const int64_t* out_offset) {
+    if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
+    if (n < 0) return fail(SFMM_INVALID_ARGUMENT, "negative batch size");
+    if (n == 0) return SFMM_OK;
+    if (!p_in || !p_out || !in || !in_offset || !shifts || !out || !out_offset)
+        return fail(SFMM_INVALID_ARGUMENT, "translation request with null solid");
+    if (kind < 0 || kind > 2) return fail(SFMM_INVALID_ARGUMENT, "unknown translation kind");
+    DeviceGuard guard(h->device);
+    if (h->precision == SFMM_F64)
+        return translate_host_mixed_impl<double>(h, kind, n, p_in, p_out, (const double*)in,
+                                                 in_offset, (const double*)shifts, (double*)out,
+                                                 out_offset);
+    return translate_host_mixed_impl<float>(h, kind, n, p_in, p_out, (const float*)in, in_offset,
+                                            (const float*)shifts, (float*)out, out_offset);
+}
+
+sfmm_status sfmm_translate_soa(sfmm_handle* h, sfmm_kind kind, int64_t n, int p_in, int p_out,
+                               const void* d_in, int64_t in_stride, const void* d_shifts,
+                               void* d_out, int64_t out_stride, void* stream, int flags) {
+    if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
+    if (n < 0) return fail(SFMM_INVALID_ARGUMENT, "negative batch size");
+    if (n == 0) return SFMM_OK;
+    if (!d_in || !d_shifts || !d_out)
+        return fail(SFMM_INVALID_ARGUMENT, "translation request with null solid");
+    if (in_stride < n || out_stride < n)
+        return fail(SFMM_INVALID_ARGUMENT, "batch stride smaller than the batch");
+    const sfmm_status st = check_orders(h, kind, p_in, p_out);
+    if (st != SFMM_OK) return st;
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (h->precision == SFMM_F64)
+        return translate_soa_impl<double>(h, kind, n, p_in, p_out, (const double*)d_in, in_stride,
+                                          (const double*)d_shifts, (double*)d_out, out_stride, s,
+                                          flags, false);
+    return translate_soa_impl<float>(h, kind, n, p_in, p_out, (const float*)d_in, in_stride,
+                                     (const float*)d_shifts, (float*)d_out, out_stride, s, flags,
+                                     false);
+}
+
+sfmm_status sfmm_stream_status(sfmm_handle* h, void* stream) {
+    if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<int> slots;
+    {
+        std::lock_guard<std::mutex> lk(h->async_mutex);
+        slots.swap(h->async_slots);
+    }
+    CU(cudaMemcpyAsync(h->h_flags, h->d_flags, sizeof(int) * kFlagSlots, cudaMemcpyDeviceToHost,
+                       s));
+    CU(cudaStreamSynchronize(s));
+    for (int slot : slots)
+        if (h->h_flags[slot]) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
+    return SFMM_OK;
+}
+
+sfmm_status sfmm_pack_soa(sfmm_handle* h, int64_t n, int p, const void* d_aos, void* d_soa,
+                          int64_t stride, void* stream) {
+    if (!h || !d_aos || !d_soa || p < 1 || n < 0 || stride < n)
+        return fail(SFMM_INVALID_ARGUMENT, "bad pack_soa arguments");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    h->launches += 1;
+    if (h->precision == SFMM_F64)
+        CU(launch_pack_soa<double>((const double*)d_aos, (double*)d_soa, n, p, stride, s));
+    else
+        CU(launch_pack_soa<float>((const float*)d_aos, (float*)d_soa, n, p, stride, s));
+    return SFMM_OK;
+}
+
+sfmm_status sfmm_unpack_soa(sfmm_handle* h, int64_t n, int p, const void* d_soa, int64_t stride,
+                            void* d_aos, void* stream) {
+    if (!h || !d_aos || !d_soa || p < 1 || n < 0 || stride < n)
+        return fail(SFMM_INVALID_ARGUMENT, "bad unpack_soa arguments");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    h->launches += 1;
+    if (h->precision == SFMM_F64)
+        CU(launch_unpack_soa<double>((const double*)d_soa, (double*)d_aos, n, p, stride, s));
+    else
+        CU(launch_unpack_soa<float>((const float*)d_soa, (float*)d_aos, n, p, stride, s));
+    return SFMM_OK;
+}
+
+sfmm_status sfmm_plan_create(sfmm_handle* h, int64_t n_targets, const int64_t* tgt_ptr,
+                             const int32_t* src_index, const void* shifts, int64_t n_sources,
+                             sfmm_plan** out) {
+    if (!out) return fail(SFMM_INVALID_ARGUMENT, "null output pointer");
+    *out = nullptr;
+    if (!h || n_targets < 0 || n_sources < 0 || !tgt_ptr)
+        return fail(SFMM_INVALID_ARGUMENT, "bad plan arguments");
+    if (tgt_ptr[0] != 0) return fail(SFMM_INVALID_ARGUMENT, "tgt_ptr[0] must be 0");
+    if (tgt_ptr[n_targets] > 0 && (!src_index || !shifts))
+        return fail(SFMM_INVALID_ARGUMENT, "translation request with null solid");
+    DeviceGuard guard(h->device);
+    auto* plan = new sfmm_plan;
+    const sfmm_status st =
+        h->precision == SFMM_F64
+            ? plan_create_impl<double>(h, n_targets, tgt_ptr, src_index, (const double*)shifts,
+                                       n_sources, plan)
+            : plan_create_impl<float>(h, n_targets, tgt_ptr, src_index, (const float*)shifts,
+                                      n_sources, plan);
+    if (st != SFMM_OK) {
+        sfmm_plan_destroy(plan);
+        return st;
+    }
+    *out = plan;
+    return SFMM_OK;
+}
+
+void sfmm_plan_destroy(sfmm_plan* plan) {
+    if (!plan) return;
+    if (plan->h) {
+        DeviceGuard guard(plan->h->device);
+        cudaFree(plan->d_grp_ptr);
+        cudaFree(plan->d_src_index);
+        cudaFree(plan->d_shifts);
+    }
+    delete plan;
+}
+
+int64_t sfmm_plan_pairs(const sfmm_plan* plan) { return plan ? plan->n_pairs : 0; }
+
+sfmm_status sfmm_m2l_accumulate(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,
+                                const void* d_src, int64_t src_stride, void* d_out,
+                                int64_t out_stride, void* stream) {
+    if (!h || !plan || plan->h != h) return fail(SFMM_INVALID_ARGUMENT, "plan/handle mismatch");
+    if (!d_src || !d_out) return fail(SFMM_INVALID_ARGUMENT, "translation request with null solid");
+    if (src_stride < plan->n_sources || out_stride < plan->n_targets)
+        return fail(SFMM_INVALID_ARGUMENT, "batch stride smaller than the batch");
+    const sfmm_status st = check_orders(h, SFMM_M2L, p_in, p_out);
+    if (st != SFMM_OK) return st;
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (h->precision == SFMM_F64)
+        return accumulate_impl<double>(h, plan, p_in, p_out, (const double*)d_src, src_stride,
+                                       (double*)d_out, out_stride, s);
+    return accumulate_impl<float>(h, plan, p_in, p_out, (const float*)d_src, src_stride,
+                                  (float*)d_out, out_stride, s);
+}
+
+sfmm_status sfmm_m2l_accumulate_host(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,
+                                     const void* src_aos, void* out_aos) {
+    if (!h || !plan || plan->h != h) return fail(SFMM_INVALID_ARGUMENT, "plan/handle mismatch");
+    if (!src_aos || !out_aos)
+        return fail(SFMM_INVALID_ARGUMENT, "translation request with null solid");
+    const sfmm_status st = check_orders(h, SFMM_M2L, p_in, p_out);
+    if (st != SFMM_OK) return st;
+    DeviceGuard guard(h->device);
+    if (h->precision == SFMM_F64)
+        return accumulate_host_impl<double>(h, plan, p_in, p_out, (const double*)src_aos,
+                                            (double*)out_aos);
+    return accumulate_host_impl<float>(h, plan, p_in, p_out, (const float*)src_aos,
+                                       (float*)out_aos);
+}
+
+}  // extern "C"

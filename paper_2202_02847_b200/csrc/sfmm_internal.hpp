@@ -1,0 +1,74 @@
+// Internal interface between the C-ABI layer (capi.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tables.hpp"
+
+namespace sfmm {
+
+enum : int { KIND_M2L = 0, KIND_M2M = 1, KIND_L2L = 2 };
+
+// Device-resident tables of one handle (precision Real).
+template <typename Real>
+struct DeviceTables {
+    int order = 0;
+    // parity-block streams: side 0 = multipole-type data (F, G),
+    // side 1 = local-type data (F^T, G^T)
+    const Real* stream[2] = {nullptr, nullptr};
+    const BlockDesc* desc[2] = {nullptr, nullptr};
+    uint32_t stream_len[2] = {0, 0};
+    const Real* fac = nullptr;   // k!, k <= 2P-2
+    const Real* inv = nullptr;   // 1/d!, d < P
+    const Real* winv = nullptr;  // (-1)^d / d!, d < P (M2M weights, pipeline.cpp:191-194)
+};
+
+// One uniform-(p_in, p_out) launch.
+template <typename Real>
+struct TranslateArgs {
+    int kind = 0;
+    int p_in = 0, p_out = 0;
+    int64_t n = 0;                // translations (lanes); in accumulate mode: padded pairs
+    const Real* in = nullptr;     // SoA [c][in_stride]
+    int64_t in_stride = 0;
+    const Real* shifts = nullptr; // [n][3]
+    Real* out = nullptr;          // SoA [c][out_stride]; accumulate mode: partials [c][n/32]
+    int64_t out_stride = 0;
+    const int32_t* src_index = nullptr;  // accumulate mode: source per lane, -1 = idle lane
+    const int* fail_flag = nullptr;      // device int; non-zero -> kernel writes nothing
+};
+
+struct LaunchInfo {
+    int grid = 0, block = 0;
+    size_t smem = 0;
+    int launches = 0;
+    const char* variant = "";
+};
+
+// Translation kernels. Returns cudaSuccess or the launch error.
+template <typename Real>
+cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Real>& a,
+                             int sm_count, cudaStream_t stream, LaunchInfo* info);
+
+// Zero-shift scan: sets *flag (device int) to 1 when any |shift| < min normal.
+template <typename Real>
+cudaError_t launch_check_shifts(const Real* shifts, int64_t n, int* flag, cudaStream_t stream);
+
+// AoS [n][P(P+1)] <-> SoA [c][stride]
+template <typename Real>
+cudaError_t launch_pack_soa(const Real* aos, Real* soa, int64_t n, int p, int64_t stride,
+                            cudaStream_t stream);
+template <typename Real>
+cudaError_t launch_unpack_soa(const Real* soa, Real* aos, int64_t n, int p, int64_t stride,
+                              cudaStream_t stream);
+
+// Accumulate mode, second stage: out[c][t] = sum_{g in groups of t} partial[c][g],
+// groups in ascending order. grp_ptr: [n_targets + 1].
+template <typename Real>
+cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const int64_t* grp_ptr,
+                                 int64_t n_targets, int p_out, Real* out, int64_t out_stride,
+                                 cudaStream_t stream);
+
+}  // namespace sfmm

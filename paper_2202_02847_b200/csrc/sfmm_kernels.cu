@@ -1,0 +1,189 @@
+// Kernel launchers (sm_100a). Compiled with -fmad=false: see device_math.cuh.
+#include <algorithm>
+
+#include "kernel_generic.cuh"
+#include "sfmm_internal.hpp"
+
+namespace sfmm {
+
+namespace {
+
+template <typename Real>
+__global__ void check_shifts_kernel(const Real* __restrict__ shifts, int64_t n, int* flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool bad = false;
+    if (i < n) bad = shift_is_degenerate(shifts[3 * i], shifts[3 * i + 1], shifts[3 * i + 2]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+// 32x32 tile transpose between AoS [b][S] and SoA [c][stride].
+template <typename Real, bool TO_SOA>
+__global__ void repack_kernel(const Real* __restrict__ src, Real* __restrict__ dst, int64_t n,
+                              int S, int64_t stride) {
+    __shared__ Real tile[32][33];
+    const int64_t b0 = (int64_t)blockIdx.x * 32;
+    const int c0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    if (TO_SOA) {
+        for (int r = ty; r < 32; r += 8) {
+            const int64_t b = b0 + r;
+            const int c = c0 + tx;
+            if (b < n && c < S) tile[r][tx] = src[b * S + c];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int c = c0 + r;
+            const int64_t b = b0 + tx;
+            if (b < n && c < S) dst[(int64_t)c * stride + b] = tile[tx][r];
+        }
+    } else {
+        for (int r = ty; r < 32; r += 8) {
+            const int c = c0 + r;
+            const int64_t b = b0 + tx;
+            if (b < n && c < S) tile[r][tx] = src[(int64_t)c * stride + b];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int64_t b = b0 + r;
+            const int c = c0 + tx;
+            if (b < n && c < S) dst[b * S + c] = tile[tx][r];
+        }
+    }
+}
+
+template <typename Real>
+__global__ void reduce_groups_kernel(const Real* __restrict__ partial, int64_t n_groups,
+                                     const int64_t* __restrict__ grp_ptr, int64_t n_targets,
+                                     int S, Real* __restrict__ out, int64_t out_stride) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (t >= n_targets) return;
+    Real acc = Real(0);
+    // Im(C_n^0) planes are never written by the translation kernel
+    int n = 0;
+    while ((n + 1) * (n + 2) <= c) ++n;
+    const bool im0 = (c == n * (n + 1) + 1);
+    if (!im0) {
+        const int64_t g0 = grp_ptr[t], g1 = grp_ptr[t + 1];
+        for (int64_t g = g0; g < g1; ++g) acc += partial[(int64_t)c * n_groups + g];
+    }
+    out[(int64_t)c * out_stride + t] = acc;
+}
+
+int g_smem_optin = -1;
+
+int smem_optin_limit() {
+    if (g_smem_optin < 0) {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        g_smem_optin = v;
+    }
+    return g_smem_optin;
+}
+
+}  // namespace
+
+template <typename Real>
+cudaError_t launch_check_shifts(const Real* shifts, int64_t n, int* flag, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int block = 256;
+    const int64_t grid = (n + block - 1) / block;
+    check_shifts_kernel<Real><<<(unsigned)grid, block, 0, stream>>>(shifts, n, flag);
+    return cudaGetLastError();
+}
+
+template <typename Real>
+cudaError_t launch_pack_soa(const Real* aos, Real* soa, int64_t n, int p, int64_t stride,
+                            cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int S = p * (p + 1);
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((S + 31) / 32)), block(32, 8);
+    repack_kernel<Real, true><<<grid, block, 0, stream>>>(aos, soa, n, S, stride);
+    return cudaGetLastError();
+}
+
+template <typename Real>
+cudaError_t launch_unpack_soa(const Real* soa, Real* aos, int64_t n, int p, int64_t stride,
+                              cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int S = p * (p + 1);
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((S + 31) / 32)), block(32, 8);
+    repack_kernel<Real, false><<<grid, block, 0, stream>>>(soa, aos, n, S, stride);
+    return cudaGetLastError();
+}
+
+template <typename Real>
+cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const int64_t* grp_ptr,
+                                 int64_t n_targets, int p_out, Real* out, int64_t out_stride,
+                                 cudaStream_t stream) {
+    if (n_targets <= 0) return cudaSuccess;
+    const int S = p_out * (p_out + 1);
+    dim3 grid((unsigned)((n_targets + 127) / 128), (unsigned)S), block(128);
+    reduce_groups_kernel<Real>
+        <<<grid, block, 0, stream>>>(partial, n_groups, grp_ptr, n_targets, S, out, out_stride);
+    return cudaGetLastError();
+}
+
+template <typename Real>
+cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Real>& a,
+                             int sm_count, cudaStream_t stream, LaunchInfo* info) {
+    if (a.n <= 0) return cudaSuccess;
+    const int p_rot = std::max(a.p_in, a.p_out);
+    const int64_t n_groups = (a.n + kLanes - 1) / kLanes;
+    const int limit = smem_optin_limit();
+
+    GenericLayout<Real> lay{p_rot, 8, true};
+    if ((int64_t)lay.smem_bytes() > limit) lay.warps = 4;
+    if ((int64_t)lay.smem_bytes() > limit) {
+        lay.warps = 8;
+        lay.buf_in_smem = false;
+    }
+    const size_t smem = lay.smem_bytes();
+    const int block = lay.warps * 32;
+
+    auto kern = lay.buf_in_smem ? translate_generic_kernel<Real, true>
+                                : translate_generic_kernel<Real, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem);
+    if (e != cudaSuccess) return e;
+    per_sm = std::max(per_sm, 1);
+    const int grid = (int)std::min<int64_t>(n_groups, (int64_t)sm_count * per_sm);
+
+    Real* gscratch = nullptr;
+    if (!lay.buf_in_smem) {
+        e = cudaMallocAsync((void**)&gscratch, sizeof(Real) * lay.buf_elems() * grid, stream);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, block, smem, stream>>>(t, a, gscratch, n_groups, p_rot);
+    e = cudaGetLastError();
+    if (gscratch) cudaFreeAsync(gscratch, stream);
+    if (info) {
+        info->grid = grid;
+        info->block = block;
+        info->smem = smem;
+        info->launches = 1;
+        info->variant = lay.buf_in_smem ? "generic/smem" : "generic/global-scratch";
+    }
+    return e;
+}
+
+#define SFMM_INSTANTIATE(Real)                                                                   \
+    template cudaError_t launch_check_shifts<Real>(const Real*, int64_t, int*, cudaStream_t);   \
+    template cudaError_t launch_pack_soa<Real>(const Real*, Real*, int64_t, int, int64_t,       \
+                                               cudaStream_t);                                   \
+    template cudaError_t launch_unpack_soa<Real>(const Real*, Real*, int64_t, int, int64_t,     \
+                                                 cudaStream_t);                                 \
+    template cudaError_t launch_reduce_groups<Real>(const Real*, int64_t, const int64_t*,       \
+                                                    int64_t, int, Real*, int64_t, cudaStream_t); \
+    template cudaError_t launch_translate<Real>(const DeviceTables<Real>&,                      \
+                                                const TranslateArgs<Real>&, int, cudaStream_t,  \
+                                                LaunchInfo*);
+
+SFMM_INSTANTIATE(double)
+SFMM_INSTANTIATE(float)
+
+}  // namespace sfmm

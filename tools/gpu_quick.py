@@ -1,0 +1,33 @@
+"""Quick GPU parity probe: CUDA library vs the CPU oracle on random requests."""
+import sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np
+from paper_2202_02847_b200 import capi
+from tests.oracle_lib import Oracle, normalized_error
+
+orc = Oracle()
+rng = np.random.default_rng(7)
+bad = 0
+for dt, prec, pmax in ((np.float64, capi.F64, 30), (np.float32, capi.F32, 18)):
+    h = capi.Handle(prec, pmax)
+    for trial in range(36):
+        kind = trial % 3
+        pin = int(rng.integers(1, pmax + 1)); pout = int(rng.integers(1, pmax + 1))
+        if trial < 6: pin = pout = [1, 2, 3, 8, pmax, pmax][trial]
+        n = int(rng.integers(1, 200))
+        x = rng.standard_normal((n, pin * (pin + 1))).astype(dt) * (0.05 if dt == np.float32 else 1)
+        for k in range(pin): x[:, k * (k + 1) + 1] = 0
+        sh = rng.standard_normal((n, 3)); sh *= rng.uniform(0.5, 2, (n, 1)) / np.linalg.norm(sh, axis=1, keepdims=True)
+        sh = sh.astype(dt)
+        if n > 4: sh[0] = [0, 0, 1.5]; sh[1] = [0, 0, -1.5]; sh[2] = [2, 0, 0]; sh[3] = [0, -1.5, 0]
+        st, want = orc.translate(kind, pin, pout, x, sh, dt)
+        assert st == 0
+        got = h.translate_host(kind, pin, pout, x, sh)
+        same = np.array_equal(got, want)
+        err = 0.0 if same else normalized_error(got, want)
+        if not same: bad += 1
+        print(f"{dt.__name__} kind={kind} p_in={pin:2d} p_out={pout:2d} n={n:3d} bit-exact={same} err={err:.2e}", flush=True)
+    h.close()
+print("MISMATCHING CASES:", bad)
+sys.exit(1 if bad else 0)
