@@ -143,6 +143,11 @@ sfmm_status sfmm_m2l_accumulate_host(sfmm_handle* h, const sfmm_plan* plan,
                                      int p_in, int p_out, const void* src_aos,
                                      void* out_aos);
 
+/* Tuning knobs without a reference counterpart. "kernel_variant": 0 = automatic
+ * (default), 1 = generic kernel (any order), 2 = tiled kernel (orders <= 20
+ * double / <= 18 single; INVALID_ARGUMENT at call time beyond that). */
+sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value);
+
 /* Number of kernel launches this handle has issued (bench.py gpu_launches). */
 int64_t sfmm_launch_count(const sfmm_handle* h);
 

@@ -17,7 +17,7 @@ CSRC = PKG_DIR / "csrc"
 INCLUDE = PKG_DIR.parent / "include"
 LIB_PATH = PKG_DIR / "libsolidfmm_b200.so"
 
-SOURCES = ["sfmm_capi.cu", "sfmm_kernels.cu", "tables.cpp"]
+SOURCES = ["sfmm_capi.cu", "sfmm_kernels.cu", "sfmm_tiled_f64.cu", "sfmm_tiled_f32.cu", "tables.cpp"]
 
 # -fmad=false: the kernels spell every fused multiply-add explicitly; nvcc must
 # not contract anything else (csrc/device_math.cuh).
@@ -42,7 +42,7 @@ def nvcc_path() -> str:
 
 
 def _inputs() -> list[Path]:
-    deps = [p for p in CSRC.iterdir() if p.suffix in (".cu", ".cuh", ".cpp", ".hpp", ".h")]
+    deps = [p for p in CSRC.iterdir() if p.suffix in (".cu", ".cuh", ".cpp", ".hpp", ".h", ".inl")]
     deps += list(INCLUDE.glob("*.h"))
     deps.append(Path(__file__))
     return deps

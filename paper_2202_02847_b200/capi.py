@@ -48,6 +48,7 @@ _SIGNATURES = {
     "sfmm_m2l_accumulate": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_int64, c_void_p,
                                     c_int64, c_void_p]),
     "sfmm_m2l_accumulate_host": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "sfmm_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
     "sfmm_launch_count": (c_int64, [c_void_p]),
 }
 
@@ -165,6 +166,9 @@ class Handle:
     @property
     def launch_count(self) -> int:
         return self._lib.sfmm_launch_count(self._h)
+
+    def set_option(self, name: str, value: int) -> None:
+        check(self._lib.sfmm_set_option(self._h, name.encode(), value))
 
     def swap_tables(self, n: int):
         f = np.empty((n + 1, n + 1), np.float64)

@@ -47,7 +47,6 @@ struct DeviceGuard {
 
 constexpr int kFlagSlots = 256;
 
-size_t elem_size(int precision) { return precision == SFMM_F64 ? 8 : 4; }
 int64_t round_up32(int64_t n) { return (n + 31) / 32 * 32; }
 int64_t solid_len(int p) { return (int64_t)p * (p + 1); }
 
@@ -69,6 +68,7 @@ struct sfmm_handle {
     std::atomic<int64_t> launches{0};
     std::mutex async_mutex;
     std::vector<int> async_slots;
+    int variant = 0;
 };
 
 struct sfmm_plan {
@@ -132,6 +132,8 @@ const DeviceTables<float>& tables_of<float>(const sfmm_handle* h) { return h->tf
 
 sfmm_status check_orders(const sfmm_handle* h, int kind, int p_in, int p_out) {
     if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
+    if (h->variant == 2 && std::max(p_in, p_out) > (h->precision == SFMM_F64 ? 20 : 18))
+        return fail(SFMM_INVALID_ARGUMENT, "tiled kernel variant does not cover this order");
     if (kind < 0 || kind > 2) return fail(SFMM_INVALID_ARGUMENT, "unknown translation kind");
     // pipeline.cpp:285-295
     if (p_in < 1 || p_out < 1)
@@ -172,6 +174,7 @@ sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, in
     a.out = d_out;
     a.out_stride = out_stride;
     a.fail_flag = d_flag;
+    a.variant = h->variant;
     LaunchInfo info;
     CU(launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info));
     h->launches += info.launches;
@@ -339,6 +342,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.out = partial;
     a.out_stride = plan->n_groups;
     a.src_index = plan->d_src_index;
+    a.variant = h->variant;
     LaunchInfo info;
     cudaError_t e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
     h->launches += info.launches;
@@ -468,6 +472,16 @@ void sfmm_destroy(sfmm_handle* h) {
 int sfmm_order(const sfmm_handle* h) { return h ? h->order : 0; }
 int sfmm_device(const sfmm_handle* h) { return h ? h->device : -1; }
 int64_t sfmm_launch_count(const sfmm_handle* h) { return h ? h->launches.load() : 0; }
+
+sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
+    if (!h || !name) return fail(SFMM_INVALID_ARGUMENT, "null handle or option name");
+    if (std::strcmp(name, "kernel_variant") == 0) {
+        if (value < 0 || value > 2) return fail(SFMM_INVALID_ARGUMENT, "kernel_variant must be 0, 1 or 2");
+        h->variant = (int)value;
+        return SFMM_OK;
+    }
+    return fail(SFMM_INVALID_ARGUMENT, std::string("unknown option ") + name);
+}
 
 sfmm_status sfmm_get_swap_tables(const sfmm_handle* h, int n, double* f, double* g) {
     if (!h || n < 0 || n >= h->order) return fail(SFMM_INVALID_ARGUMENT, "row out of range");

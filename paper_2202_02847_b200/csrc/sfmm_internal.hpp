@@ -38,6 +38,7 @@ struct TranslateArgs {
     int64_t out_stride = 0;
     const int32_t* src_index = nullptr;  // accumulate mode: source per lane, -1 = idle lane
     const int* fail_flag = nullptr;      // device int; non-zero -> kernel writes nothing
+    int variant = 0;                     // 0 auto, 1 generic kernel, 2 tiled kernel
 };
 
 struct LaunchInfo {
@@ -51,6 +52,14 @@ struct LaunchInfo {
 template <typename Real>
 cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Real>& a,
                              int sm_count, cudaStream_t stream, LaunchInfo* info);
+
+// Tuned kernels (kernel_tiled.inl): orders <= 20 (double) / <= 18 (float).
+bool tiled_supports(const TranslateArgs<double>& a);
+bool tiled_supports(const TranslateArgs<float>& a);
+cudaError_t launch_translate_tiled(const TranslateArgs<double>& a, int sm_count,
+                                   cudaStream_t stream, LaunchInfo* info);
+cudaError_t launch_translate_tiled(const TranslateArgs<float>& a, int sm_count,
+                                   cudaStream_t stream, LaunchInfo* info);
 
 // Zero-shift scan: sets *flag (device int) to 1 when any |shift| < min normal.
 template <typename Real>

@@ -171,6 +171,40 @@ __global__ void k_block_const(double* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = total;
 }
 
+// ---- 4b. as 4, but the base offset is not provably warp-uniform, so ptxas emits
+// LDC (vector-register address) instead of LDCU (uniform datapath)
+template <int NO, int NI, int TL>
+__global__ void k_block_const_v(double* out, int iters, const int* __restrict__ zero) {
+    double x[NI][TL], acc[NO][TL];
+#pragma unroll
+    for (int k = 0; k < NI; ++k)
+#pragma unroll
+        for (int t = 0; t < TL; ++t) x[k][t] = threadIdx.x * 0.001 + k + t;
+    double total = 0;
+    constexpr int BLK = NO * NI;
+    const int z = __shfl_sync(0xffffffffu, zero[threadIdx.x >> 5], 0);
+    for (int it = 0; it < iters; ++it) {
+        for (int base0 = 0; base0 + BLK <= TAB; base0 += BLK) {
+            const int base = base0 + z;
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+#pragma unroll
+                for (int t = 0; t < TL; ++t) acc[i][t] = 0;
+#pragma unroll
+            for (int e = 0; e < BLK; ++e) {
+                const double a = c_tab[base + e];
+#pragma unroll
+                for (int t = 0; t < TL; ++t) acc[e % NO][t] = fma(a, x[e / NO][t], acc[e % NO][t]);
+            }
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+#pragma unroll
+                for (int t = 0; t < TL; ++t) total += acc[i][t];
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = total;
+}
+
 // ---- 5. shared-memory data traffic: per-lane LDS.64/STS.64 on a [q][32] column
 __global__ void k_lds_stream(double* out, int iters) {
     extern __shared__ double buf[];
@@ -284,7 +318,7 @@ int main(int argc, char** argv) {
     for (int warps : {4, 8, 12, 16}) {
         run_lds(k_block_lds<10, 10, 1>, "block_lds", 10, 10, 1, warps);
         run_lds(k_block_lds<10, 10, 2>, "block_lds", 10, 10, 2, warps);
-        run_lds(k_block_lds<10, 10, 4>, "block_lds", 10, 10, 4, warps);
+        if (warps <= 12) run_lds(k_block_lds<10, 10, 4>, "block_lds", 10, 10, 4, warps);
         run_lds(k_block_lds<6, 6, 2>, "block_lds", 6, 6, 2, warps);
     }
     auto run_const = [&](auto kern, int NO, int NI, int TL, int warps) {
@@ -300,7 +334,19 @@ int main(int argc, char** argv) {
         run_const(k_block_const<10, 10, 1>, 10, 10, 1, warps);
         run_const(k_block_const<10, 10, 2>, 10, 10, 2, warps);
     }
-    for (int warps : {4, 8, 16, 32}) {
+    {
+        int* zero;
+        CK(cudaMalloc(&zero, 256));
+        CK(cudaMemset(zero, 0, 256));
+        for (int warps : {8, 12, 16}) {
+            const int block = warps * 32, grid = sms, iters = 64;
+            float ms = time_ms([&] { k_block_const_v<10, 10, 2><<<grid, block>>>(out, iters, zero); });
+            double fl = 2.0 * 100 * 2 * (TAB / 100) * (double)iters * grid * block;
+            printf("{\"test\": \"block_const_vectorLDC\", \"NO\": 10, \"NI\": 10, \"TL\": 2, \"warps_per_sm\": %d, "
+                   "\"ms\": %.3f, \"tflops\": %.2f}\n", warps, ms, fl / ms * 1e-9);
+        }
+    }
+    for (int warps : {4, 8, 16}) {
         const int block = warps * 32, grid = sms, iters = 2000;
         const size_t smem = (size_t)warps * 64 * 32 * 8;
         CK(cudaFuncSetAttribute(k_lds_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
