@@ -148,6 +148,11 @@ sfmm_status sfmm_m2l_accumulate_host(sfmm_handle* h, const sfmm_plan* plan,
  * double / <= 18 single; INVALID_ARGUMENT at call time beyond that). */
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value);
 
+/* Measures the FMA-pipe peak (TFLOP/s, 2 flops per FMA) of the handle's device
+ * in the handle's precision with a register-only kernel (~10 ms). Benchmarks
+ * use it as the compute-roofline denominator. */
+sfmm_status sfmm_measure_fma_peak(sfmm_handle* h, double* tflops);
+
 /* Number of kernel launches this handle has issued (bench.py gpu_launches). */
 int64_t sfmm_launch_count(const sfmm_handle* h);
 

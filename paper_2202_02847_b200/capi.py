@@ -49,6 +49,7 @@ _SIGNATURES = {
                                     c_int64, c_void_p]),
     "sfmm_m2l_accumulate_host": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "sfmm_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
+    "sfmm_measure_fma_peak": (c_int, [c_void_p, POINTER(c_double)]),
     "sfmm_launch_count": (c_int64, [c_void_p]),
 }
 
@@ -169,6 +170,11 @@ class Handle:
 
     def set_option(self, name: str, value: int) -> None:
         check(self._lib.sfmm_set_option(self._h, name.encode(), value))
+
+    def measure_fma_peak(self) -> float:
+        v = c_double(0)
+        check(self._lib.sfmm_measure_fma_peak(self._h, ctypes.byref(v)))
+        return v.value
 
     def swap_tables(self, n: int):
         f = np.empty((n + 1, n + 1), np.float64)

@@ -68,6 +68,12 @@ constexpr int RM_BASE = SWAP_LEN + SWAP_PAD;
 
 __device__ __forceinline__ int class_size(int n, int cls) { return cls ? (n + 1) >> 1 : (n >> 1) + 1; }
 
+// Shared-memory triangle of the tiled kernel: row n starts at n^2 and holds
+// re_l at 2l and im_l (l >= 1) at 2l-1, so both parts of a parity class are
+// reached from one base with compile-time strides.
+__device__ __forceinline__ int t_re(int n, int l) { return n * n + 2 * l; }
+__device__ __forceinline__ int t_im(int n, int l) { return n * n + 2 * l - 1; }
+
 template <int TL>
 struct Ctx {
     Real* buf;       // lane offset applied; element q, slot t at buf[q * L + 32 t]
@@ -78,72 +84,232 @@ struct Ctx {
 
 // One parity half of swap -> rotate(+-beta) -> swap on row n (reference
 // pipeline.cpp:118-136 with :155-157 / :247-249), in place in shared memory.
+//
+// For the intermediate class `cls` of size NC the real-part blocks are always
+// NC x NC; the imaginary-part blocks are NC x nG and nG x NC with
+// nG = NC-1, NC or NC+1, of which NC-1 or NC indices are usable (l = 0 carries
+// no imaginary part). Everything is straight-line code in NC so that ptxas can
+// hoist the constant-bank and shared-memory loads ahead of the FMA chains.
 template <int TL, int NC>
-__device__ __forceinline__ void half_task(const Ctx<TL>& c, int n, int cls, int mmax) {
+__device__ __forceinline__ void half_task_fast(const Ctx<TL>& c, int n, int cls) {
+    constexpr int L = 32 * TL;
+    const int cF = (n - cls) & 1, cG = cF ^ 1;
+    const int nG = class_size(n, cG);
+    const int g0 = cG ? 0 : 1;  // first usable index of the imaginary class
+    const int nGe = nG - g0;    // NC-1 or NC
+    const int offF_cls = c_blk[n * 4 + cls], offG_cls = c_blk[n * 4 + 2 + cls];
+    const int offF_cF = c_blk[n * 4 + cF], offG_cG = c_blk[n * 4 + 2 + cG];
+    // index = base + k * ld + i with k the contracted index in both products
+    const int f1 = c.local_side ? RM_BASE + offF_cF : offF_cls;
+    const int g1 = (c.local_side ? RM_BASE + offG_cG : offG_cls) + g0 * NC;
+    const int f2 = c.local_side ? RM_BASE + offF_cls : offF_cF;
+    const int g2 = (c.local_side ? RM_BASE + offG_cls : offG_cG) + g0;
+    Real* row = c.buf + n * n * L;
+    Real* re_in = row + (2 * cF) * L;               // + 4k L
+    Real* im_in = row + (2 * (cG + 2 * g0) - 1) * L;  // + 4k L
+
+    Real ure[NC][TL], uim[NC][TL];
+    // ---- first product, real parts
+    {
+        Real x[NC][TL];
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) x[k][t] = re_in[4 * k * L + 32 * t];
+        if (c.local_side && cF == 0) {
+#pragma unroll
+            for (int t = 0; t < TL; ++t) x[0][t] *= Real(0.5);
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) ure[i][t] = Real(0);
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const Real a = c_sw[f1 + k * NC + i];
+#pragma unroll
+                for (int t = 0; t < TL; ++t) ure[i][t] = fma_(a, x[k][t], ure[i][t]);
+            }
+    }
+    // ---- first product, imaginary parts (NC-1 inputs always, one more if nGe == NC)
+    {
+        Real x[NC][TL];
+#pragma unroll
+        for (int k = 0; k < NC - 1; ++k)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) x[k][t] = im_in[4 * k * L + 32 * t];
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) uim[i][t] = Real(0);
+#pragma unroll
+        for (int k = 0; k < NC - 1; ++k)
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const Real a = c_sw[g1 + k * NC + i];
+#pragma unroll
+                for (int t = 0; t < TL; ++t) uim[i][t] = fma_(a, x[k][t], uim[i][t]);
+            }
+        if (nGe == NC) {
+            constexpr int k = NC - 1;
+#pragma unroll
+            for (int t = 0; t < TL; ++t) x[k][t] = im_in[4 * k * L + 32 * t];
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const Real a = c_sw[g1 + k * NC + i];
+#pragma unroll
+                for (int t = 0; t < TL; ++t) uim[i][t] = fma_(a, x[k][t], uim[i][t]);
+            }
+        }
+    }
+    // ---- M2L backward gather signs (-1)^(n+l) (pipeline.cpp:235-239): constant
+    // over a parity class, so they are applied to the products instead of the inputs
+    if (c.with_signs) {
+        if (cls) {
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int t = 0; t < TL; ++t) ure[i][t] = -ure[i][t];
+        } else {
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int t = 0; t < TL; ++t) uim[i][t] = -uim[i][t];
+        }
+    }
+    // ---- rotate by +-beta (kernels.cpp:211-217)
+    {
+        const Real* cbp = c.cb + cls * L;
+        const Real* sbp = c.sb + cls * L;
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                const Real cm = cbp[2 * i * L + 32 * t];
+                Real sm = sbp[2 * i * L + 32 * t];
+                if (c.negate_sb) sm = -sm;
+                const Real a = ure[i][t], b = uim[i][t];
+                ure[i][t] = fma_(a, cm, -(b * sm));
+                uim[i][t] = fma_(a, sm, b * cm);
+            }
+    }
+    // ---- second product, real parts: outputs m' = cF + 2i
+    {
+        Real acc[NC][TL];
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) acc[i][t] = Real(0);
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const Real a = c_sw[f2 + k * NC + i];
+#pragma unroll
+                for (int t = 0; t < TL; ++t) acc[i][t] = fma_(a, ure[k][t], acc[i][t]);
+            }
+        if (c.local_side && cF == 0) {
+#pragma unroll
+            for (int t = 0; t < TL; ++t) acc[0][t] *= Real(2);
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) re_in[4 * i * L + 32 * t] = acc[i][t];
+    }
+    // ---- second product, imaginary parts: outputs m' = cG + 2(i + g0), i < nGe
+    {
+        Real acc[NC][TL];
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) acc[i][t] = Real(0);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            const int b = g2 + k * nG;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const Real a = c_sw[b + i];
+#pragma unroll
+                for (int t = 0; t < TL; ++t) acc[i][t] = fma_(a, uim[k][t], acc[i][t]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NC - 1; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) im_in[4 * i * L + 32 * t] = acc[i][t];
+        if (nGe == NC) {
+#pragma unroll
+            for (int t = 0; t < TL; ++t) im_in[4 * (NC - 1) * L + 32 * t] = acc[NC - 1][t];
+        }
+    }
+}
+
+// Same half task with runtime trip counts: used only for backward rows whose
+// inputs are truncated (columns >= min(p_in, p_out) are zero, reference
+// pipeline.cpp:229-246), i.e. for p_out > p_in.
+template <int TL, int NC>
+__device__ __noinline__ void half_task_slow(const Ctx<TL>& c, int n, int cls, int mmax) {
     constexpr int L = 32 * TL;
     const int cF = (n - cls) & 1, cG = cF ^ 1;
     const int nF = class_size(n, cF), nG = class_size(n, cG);
     const int offF_cls = c_blk[n * 4 + cls], offG_cls = c_blk[n * 4 + 2 + cls];
     const int offF_cF = c_blk[n * 4 + cF], offG_cG = c_blk[n * 4 + 2 + cG];
-    // table bases: index = base + outer * NC + inner for both products
     const int f1 = c.local_side ? RM_BASE + offF_cF : offF_cls;
     const int g1 = c.local_side ? RM_BASE + offG_cG : offG_cls;
-    const int f2 = c.local_side ? offF_cls : RM_BASE + offF_cF;
-    const int g2 = c.local_side ? offG_cls : RM_BASE + offG_cG;
+    const int f2 = c.local_side ? RM_BASE + offF_cls : offF_cF;
+    const int g2 = c.local_side ? RM_BASE + offG_cls : offG_cG;
 
     Real ure[NC][TL], uim[NC][TL];
 #pragma unroll
     for (int i = 0; i < NC; ++i)
 #pragma unroll
         for (int t = 0; t < TL; ++t) ure[i][t] = uim[i][t] = Real(0);
-
-    // ---- first product, real parts: inputs l = cF + 2k, l <= mmax
     {
         const int kend = mmax >= cF ? min(nF, ((mmax - cF) >> 1) + 1) : 0;
         for (int k = 0; k < kend; ++k) {
             const int l = cF + 2 * k;
             Real x[TL];
 #pragma unroll
-            for (int t = 0; t < TL; ++t) x[t] = c.buf[q_re(n, l) * L + 32 * t];
-            if (c.with_signs && ((n + l) & 1)) {
-#pragma unroll
-                for (int t = 0; t < TL; ++t) x[t] = -x[t];
-            }
+            for (int t = 0; t < TL; ++t) x[t] = c.buf[t_re(n, l) * L + 32 * t];
             if (c.local_side && l == 0) {
 #pragma unroll
                 for (int t = 0; t < TL; ++t) x[t] *= Real(0.5);
             }
-            const int b = f1 + k * NC;
 #pragma unroll
             for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[b + i];
+                const Real a = c_sw[f1 + k * NC + i];
 #pragma unroll
                 for (int t = 0; t < TL; ++t) ure[i][t] = fma_(a, x[t], ure[i][t]);
             }
         }
     }
-    // ---- first product, imaginary parts: inputs l = cG + 2k, l >= 1
     {
         const int kend = mmax >= cG ? min(nG, ((mmax - cG) >> 1) + 1) : 0;
         for (int k = cG ? 0 : 1; k < kend; ++k) {
             const int l = cG + 2 * k;
             Real x[TL];
 #pragma unroll
-            for (int t = 0; t < TL; ++t) x[t] = c.buf[q_im(n, l) * L + 32 * t];
-            if (c.with_signs && ((n + l) & 1)) {
-#pragma unroll
-                for (int t = 0; t < TL; ++t) x[t] = -x[t];
-            }
-            const int b = g1 + k * NC;
+            for (int t = 0; t < TL; ++t) x[t] = c.buf[t_im(n, l) * L + 32 * t];
 #pragma unroll
             for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[b + i];
+                const Real a = c_sw[g1 + k * NC + i];
 #pragma unroll
                 for (int t = 0; t < TL; ++t) uim[i][t] = fma_(a, x[t], uim[i][t]);
             }
         }
     }
-    // ---- rotate by +-beta (kernels.cpp:211-217)
+    if (c.with_signs) {
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                if (cls) ure[i][t] = -ure[i][t];
+                else uim[i][t] = -uim[i][t];
+            }
+    }
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
         const int m = cls + 2 * i;
@@ -157,69 +323,51 @@ __device__ __forceinline__ void half_task(const Ctx<TL>& c, int n, int cls, int 
             uim[i][t] = fma_(a, sm, b * cm);
         }
     }
-    // ---- second product, real parts: outputs m' = cF + 2i, four at a time
-    for (int i0 = 0; i0 < nF; i0 += 4) {
-        Real acc[4][TL];
+    for (int i = 0; i < nF; ++i) {
+        Real acc[TL];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int t = 0; t < TL; ++t) acc[t] = Real(0);
 #pragma unroll
-            for (int t = 0; t < TL; ++t) acc[j][t] = Real(0);
-        const int b = f2 + i0 * NC;
+        for (int k = 0; k < NC; ++k) {
+            const Real a = c_sw[f2 + k * nF + i];
 #pragma unroll
-        for (int k = 0; k < NC; ++k)
+            for (int t = 0; t < TL; ++t) acc[t] = fma_(a, ure[k][t], acc[t]);
+        }
+        const int m = cF + 2 * i;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const Real a = c_sw[b + j * NC + k];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) acc[j][t] = fma_(a, ure[k][t], acc[j][t]);
-            }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (i0 + j < nF) {
-                const int m = cF + 2 * (i0 + j);
-#pragma unroll
-                for (int t = 0; t < TL; ++t) {
-                    Real v = acc[j][t];
-                    if (c.local_side && m == 0) v *= Real(2);
-                    c.buf[q_re(n, m) * L + 32 * t] = v;
-                }
-            }
+        for (int t = 0; t < TL; ++t) {
+            Real v = acc[t];
+            if (c.local_side && m == 0) v *= Real(2);
+            c.buf[t_re(n, m) * L + 32 * t] = v;
         }
     }
-    // ---- second product, imaginary parts: outputs m' = cG + 2i, m' >= 1
-    for (int i0 = 0; i0 < nG; i0 += 4) {
-        Real acc[4][TL];
+    for (int i = cG ? 0 : 1; i < nG; ++i) {
+        Real acc[TL];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int t = 0; t < TL; ++t) acc[t] = Real(0);
 #pragma unroll
-            for (int t = 0; t < TL; ++t) acc[j][t] = Real(0);
-        const int b = g2 + i0 * NC;
+        for (int k = 0; k < NC; ++k) {
+            const Real a = c_sw[g2 + k * nG + i];
 #pragma unroll
-        for (int k = 0; k < NC; ++k)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const Real a = c_sw[b + j * NC + k];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) acc[j][t] = fma_(a, uim[k][t], acc[j][t]);
-            }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int m = cG + 2 * (i0 + j);
-            if (i0 + j < nG && m != 0) {
-#pragma unroll
-                for (int t = 0; t < TL; ++t) c.buf[q_im(n, m) * L + 32 * t] = acc[j][t];
-            }
+            for (int t = 0; t < TL; ++t) acc[t] = fma_(a, uim[k][t], acc[t]);
         }
+        const int m = cG + 2 * i;
+#pragma unroll
+        for (int t = 0; t < TL; ++t) c.buf[t_im(n, m) * L + 32 * t] = acc[t];
     }
 }
 
 template <int TL>
 __device__ __forceinline__ void half_task_dispatch(const Ctx<TL>& c, int n, int cls, int mmax) {
     const int nc = class_size(n, cls);
+    const bool full = mmax >= n;
     switch (nc) {
-#define SFMM_CASE(K)                                 \
-    case K:                                          \
-        if constexpr (K <= NCMAX) half_task<TL, K>(c, n, cls, mmax); \
+#define SFMM_CASE(K)                                        \
+    case K:                                                 \
+        if constexpr (K <= NCMAX) {                         \
+            if (full) half_task_fast<TL, K>(c, n, cls);     \
+            else half_task_slow<TL, K>(c, n, cls, mmax);    \
+        }                                                   \
         break;
         SFMM_CASE(1) SFMM_CASE(2) SFMM_CASE(3) SFMM_CASE(4) SFMM_CASE(5)
         SFMM_CASE(6) SFMM_CASE(7) SFMM_CASE(8) SFMM_CASE(9) SFMM_CASE(10)
@@ -228,39 +376,57 @@ __device__ __forceinline__ void half_task_dispatch(const Ctx<TL>& c, int n, int 
     }
 }
 
-// z-axis step on column (m, part) in place; R accumulators (outputs) per
-// translation (reference kernels.cpp:118-196).
-template <int TL, int R>
-__device__ __forceinline__ void zstep_task(Real* buf, int kind, int p_in, int p_out, int m,
+// z-axis step on column (m, part) in place, R outputs per translation
+// (reference kernels.cpp:118-196). The operator is Hankel (M2L: (2m+i+k)!) or
+// Toeplitz (M2M/L2L), so four k-steps share one sliding window of R+3 entries.
+template <int TL, int R, int DIR>
+__device__ __forceinline__ void zstep_task(Real* buf, int zi, int p_in, int p_out, int m,
                                            int part) {
     constexpr int L = 32 * TL;
     const int kin = p_in - m, kout = p_out - m;
+    Real* col = buf + (part ? t_im(m, m) : t_re(m, m)) * L;  // element k at col[(2 m k + k^2) L]
     Real acc[R][TL];
 #pragma unroll
     for (int i = 0; i < R; ++i)
 #pragma unroll
         for (int t = 0; t < TL; ++t) acc[i][t] = Real(0);
-    int zi = kind == KIND_M2L ? Z_FAC + 2 * m : (kind == KIND_M2M ? Z_LOW + PMAX : Z_UP + PMAX);
-    const int zstep = kind == KIND_M2L ? 1 : -1;
-    for (int k = 0; k < kin; ++k) {
-        Real x[TL];
-        const int q = part ? q_im(m + k, m) : q_re(m + k, m);
+    int k = 0;
+    for (; k + 4 <= kin; k += 4) {
+        Real w[R + 3];
+        const int w0 = DIR > 0 ? zi : zi - 3;
 #pragma unroll
-        for (int t = 0; t < TL; ++t) x[t] = buf[q * L + 32 * t];
+        for (int j = 0; j < R + 3; ++j) w[j] = c_z[w0 + j];
+        Real x[4][TL];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) x[u][t] = col[((2 * m + k + u) * (k + u)) * L + 32 * t];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+#pragma unroll
+                for (int t = 0; t < TL; ++t)
+                    acc[i][t] = fma_(w[(DIR > 0 ? u : 3 - u) + i], x[u][t], acc[i][t]);
+        zi += 4 * DIR;
+    }
+    for (; k < kin; ++k) {
+        Real x[TL];
+#pragma unroll
+        for (int t = 0; t < TL; ++t) x[t] = col[((2 * m + k) * k) * L + 32 * t];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             const Real a = c_z[zi + i];
 #pragma unroll
             for (int t = 0; t < TL; ++t) acc[i][t] = fma_(a, x[t], acc[i][t]);
         }
-        zi += zstep;
+        zi += DIR;
     }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
         if (i < kout) {
-            const int q = part ? q_im(m + i, m) : q_re(m + i, m);
 #pragma unroll
-            for (int t = 0; t < TL; ++t) buf[q * L + 32 * t] = acc[i][t];
+            for (int t = 0; t < TL; ++t) col[((2 * m + i) * i) * L + 32 * t] = acc[i][t];
         }
     }
 }
@@ -269,10 +435,14 @@ template <int TL>
 __device__ __forceinline__ void zstep_dispatch(Real* buf, int kind, int p_in, int p_out, int m,
                                                int part) {
     const int r4 = (p_out - m + 3) >> 2;
+    const int zi = kind == KIND_M2L ? Z_FAC + 2 * m : (kind == KIND_M2M ? Z_LOW + PMAX : Z_UP + PMAX);
     switch (r4) {
-#define SFMM_CASE(K)                                                                   \
-    case K:                                                                            \
-        if constexpr (4 * K <= PMAX + 3) zstep_task<TL, 4 * K>(buf, kind, p_in, p_out, m, part); \
+#define SFMM_CASE(K)                                                                  \
+    case K:                                                                           \
+        if constexpr (4 * K <= PMAX + 3) {                                            \
+            if (kind == KIND_M2L) zstep_task<TL, 4 * K, 1>(buf, zi, p_in, p_out, m, part);  \
+            else zstep_task<TL, 4 * K, -1>(buf, zi, p_in, p_out, m, part);            \
+        }                                                                             \
         break;
         SFMM_CASE(1) SFMM_CASE(2) SFMM_CASE(3) SFMM_CASE(4) SFMM_CASE(5)
 #undef SFMM_CASE
@@ -297,10 +467,23 @@ struct TiledLayout {
     }
 };
 
+// Column-major walk over the triangle (n, m), n >= m, of order p: the element
+// order of phases A and D.
+struct TriWalk {
+    int n, m, p;
+    __device__ __forceinline__ void advance() {
+        if (++n == p) {
+            ++m;
+            n = m;
+        }
+    }
+};
+
 template <int TL>
 __global__ void __launch_bounds__(384, 1)
 translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
     constexpr int L = 32 * TL;
+    constexpr int CH = 4;  // elements whose global loads are issued together
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (a.fail_flag && *a.fail_flag) return;
 
@@ -334,6 +517,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
                 src[t] = a.src_index[b[t]];
                 active[t] = src[t] >= 0;
             }
+            if (!active[t]) src[t] = 0;
         }
 
         // ---- G: geometry tables (pipeline.cpp:52-91), one warp per slot set
@@ -372,12 +556,15 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
             const int T = p_in * (p_in + 1) / 2;
             int e = (int)((long)T * warp / W);
             const int e_end = (int)((long)T * (warp + 1) / W);
-            int m = 0, rem = e;
-            while (rem >= p_in - m) {
-                rem -= p_in - m;
-                ++m;
+            TriWalk w{0, 0, p_in};
+            {
+                int rem = e;
+                while (rem >= p_in - w.m) {
+                    rem -= p_in - w.m;
+                    ++w.m;
+                }
+                w.n = w.m + rem;
             }
-            int n = m + rem;
             Real c1[TL], s1[TL], base[TL], c[TL], s[TL], qcol[TL], q[TL];
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
@@ -386,7 +573,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
                 base[t] = src_local ? geo[2 * L + 32 * t] : geo[3 * L + 32 * t];
                 c[t] = 1;
                 s[t] = 0;
-                for (int j = 0; j < m; ++j) {
+                for (int j = 0; j < w.m; ++j) {
                     const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));
                     const Real ns = fma_(s[t], c1[t], c[t] * s1[t]);
                     c[t] = nc;
@@ -395,37 +582,53 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
                 // scale of element (n, m): |r|^n for local sources, |r|^-(n+1) otherwise,
                 // by repeated multiplication from 1 (pipeline.cpp:81-89)
                 qcol[t] = 1;
-                for (int j = 0; j < (src_local ? m : m + 1); ++j) qcol[t] *= base[t];
+                for (int j = 0; j < (src_local ? w.m : w.m + 1); ++j) qcol[t] *= base[t];
                 q[t] = qcol[t];
-                for (int j = m; j < n; ++j) q[t] *= base[t];
+                for (int j = w.m; j < w.n; ++j) q[t] *= base[t];
             }
-            for (; e < e_end; ++e) {
+            while (e < e_end) {
+                const int cnt = min(CH, e_end - e);
+                Real re[CH][TL], im[CH][TL];
+                TriWalk wl = w;
 #pragma unroll
-                for (int t = 0; t < TL; ++t) {
-                    Real re = 0, im = 0;
-                    if (active[t]) {
-                        re = a.in[(int64_t)aos_re(n, m) * a.in_stride + src[t]];
-                        if (m) im = a.in[(int64_t)(aos_re(n, m) + 1) * a.in_stride + src[t]];
-                    }
-                    const Real nr = q[t] * fma_(re, c[t], -(im * s[t]));
-                    const Real ni = q[t] * fma_(re, s[t], im * c[t]);
-                    buf[q_re(n, m) * L + 32 * t] = nr;
-                    if (m) buf[q_im(n, m) * L + 32 * t] = ni;
-                    q[t] *= base[t];
-                }
-                if (++n == p_in) {
-                    ++m;
-                    n = m;
+                for (int u = 0; u < CH; ++u) {
+                    if (u < cnt) {
+                        const int64_t off = (int64_t)aos_re(wl.n, wl.m) * a.in_stride;
 #pragma unroll
-                    for (int t = 0; t < TL; ++t) {
-                        const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));
-                        const Real ns = fma_(s[t], c1[t], c[t] * s1[t]);
-                        c[t] = nc;
-                        s[t] = ns;
-                        qcol[t] *= base[t];
-                        q[t] = qcol[t];
+                        for (int t = 0; t < TL; ++t) {
+                            re[u][t] = active[t] ? a.in[off + src[t]] : Real(0);
+                            im[u][t] = (active[t] && wl.m) ? a.in[off + a.in_stride + src[t]] : Real(0);
+                        }
+                        wl.advance();
                     }
                 }
+#pragma unroll
+                for (int u = 0; u < CH; ++u) {
+                    if (u < cnt) {
+#pragma unroll
+                        for (int t = 0; t < TL; ++t) {
+                            const Real nr = q[t] * fma_(re[u][t], c[t], -(im[u][t] * s[t]));
+                            const Real ni = q[t] * fma_(re[u][t], s[t], im[u][t] * c[t]);
+                            buf[t_re(w.n, w.m) * L + 32 * t] = nr;
+                            if (w.m) buf[t_im(w.n, w.m) * L + 32 * t] = ni;
+                            q[t] *= base[t];
+                        }
+                        const int m_before = w.m;
+                        w.advance();
+                        if (w.m != m_before) {
+#pragma unroll
+                            for (int t = 0; t < TL; ++t) {
+                                const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));
+                                const Real ns = fma_(s[t], c1[t], c[t] * s1[t]);
+                                c[t] = nc;
+                                s[t] = ns;
+                                qcol[t] *= base[t];
+                                q[t] = qcol[t];
+                            }
+                        }
+                    }
+                }
+                e += cnt;
             }
         }
         __syncthreads();
@@ -467,12 +670,15 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
             const int T = p_out * (p_out + 1) / 2;
             int e = (int)((long)T * warp / W);
             const int e_end = (int)((long)T * (warp + 1) / W);
-            int m = 0, rem = e;
-            while (rem >= p_out - m) {
-                rem -= p_out - m;
-                ++m;
+            TriWalk w{0, 0, p_out};
+            {
+                int rem = e;
+                while (rem >= p_out - w.m) {
+                    rem -= p_out - w.m;
+                    ++w.m;
+                }
+                w.n = w.m + rem;
             }
-            int n = m + rem;
             Real c1[TL], s1[TL], base[TL], c[TL], s[TL], qcol[TL], q[TL];
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
@@ -481,7 +687,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
                 base[t] = dst_local ? geo[3 * L + 32 * t] : geo[2 * L + 32 * t];
                 c[t] = 1;
                 s[t] = 0;
-                for (int j = 0; j < m; ++j) {
+                for (int j = 0; j < w.m; ++j) {
                     const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));
                     const Real ns = fma_(s[t], c1[t], c[t] * s1[t]);
                     c[t] = nc;
@@ -489,16 +695,17 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
                 }
                 // |r|^-n for local targets, |r|^(n+1) for multipole targets
                 qcol[t] = 1;
-                for (int j = 0; j < (dst_local ? m : m + 1); ++j) qcol[t] *= base[t];
+                for (int j = 0; j < (dst_local ? w.m : w.m + 1); ++j) qcol[t] *= base[t];
                 q[t] = qcol[t];
-                for (int j = m; j < n; ++j) q[t] *= base[t];
+                for (int j = w.m; j < w.n; ++j) q[t] *= base[t];
             }
             for (; e < e_end; ++e) {
+                const int n = w.n, m = w.m;
                 Real nr[TL], ni[TL];
 #pragma unroll
                 for (int t = 0; t < TL; ++t) {
-                    const Real re = buf[q_re(n, m) * L + 32 * t];
-                    const Real im = m ? buf[q_im(n, m) * L + 32 * t] : Real(0);
+                    const Real re = buf[t_re(n, m) * L + 32 * t];
+                    const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
                     const Real ms = -s[t];
                     nr[t] = q[t] * fma_(re, c[t], -(im * ms));
                     ni[t] = q[t] * fma_(re, ms, im * c[t]);
@@ -527,9 +734,8 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
                         if (m) a.out[(int64_t)(aos_re(n, m) + 1) * a.out_stride + g] = si;
                     }
                 }
-                if (++n == p_out) {
-                    ++m;
-                    n = m;
+                w.advance();
+                if (w.m != m) {
 #pragma unroll
                     for (int t = 0; t < TL; ++t) {
                         const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));

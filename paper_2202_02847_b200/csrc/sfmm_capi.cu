@@ -473,6 +473,17 @@ int sfmm_order(const sfmm_handle* h) { return h ? h->order : 0; }
 int sfmm_device(const sfmm_handle* h) { return h ? h->device : -1; }
 int64_t sfmm_launch_count(const sfmm_handle* h) { return h ? h->launches.load() : 0; }
 
+sfmm_status sfmm_measure_fma_peak(sfmm_handle* h, double* tflops) {
+    if (!h || !tflops) return fail(SFMM_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(h->device);
+    if (h->precision == SFMM_F64)
+        CU(measure_fma_peak<double>(h->sm_count, tflops));
+    else
+        CU(measure_fma_peak<float>(h->sm_count, tflops));
+    h->launches += 4;
+    return SFMM_OK;
+}
+
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
     if (!h || !name) return fail(SFMM_INVALID_ARGUMENT, "null handle or option name");
     if (std::strcmp(name, "kernel_variant") == 0) {

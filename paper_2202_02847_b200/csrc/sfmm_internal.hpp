@@ -61,6 +61,10 @@ cudaError_t launch_translate_tiled(const TranslateArgs<double>& a, int sm_count,
 cudaError_t launch_translate_tiled(const TranslateArgs<float>& a, int sm_count,
                                    cudaStream_t stream, LaunchInfo* info);
 
+// Measured FMA-pipe peak of the current device in the given precision.
+template <typename Real>
+cudaError_t measure_fma_peak(int sm_count, double* tflops);
+
 // Zero-shift scan: sets *flag (device int) to 1 when any |shift| < min normal.
 template <typename Real>
 cudaError_t launch_check_shifts(const Real* shifts, int64_t n, int* flag, cudaStream_t stream);

@@ -70,6 +70,24 @@ __global__ void reduce_groups_kernel(const Real* __restrict__ partial, int64_t n
     out[(int64_t)c * out_stride + t] = acc;
 }
 
+// FMA-pipe peak probe (roofline denominator measured next to the benchmark).
+template <typename Real>
+__global__ void fma_peak_kernel(Real* out, int iters, Real a, Real b) {
+    Real x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = Real(threadIdx.x + j);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = fma_(x[j], a, b);
+    }
+    Real s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += x[j];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int g_smem_optin = -1;
 
 int smem_optin_limit() {
@@ -83,6 +101,36 @@ int smem_optin_limit() {
 }
 
 }  // namespace
+
+template <typename Real>
+cudaError_t measure_fma_peak(int sm_count, double* tflops) {
+    const int block = 256, grid = sm_count * 4, iters = 4096;
+    Real* out = nullptr;
+    cudaError_t e = cudaMalloc((void**)&out, sizeof(Real) * (size_t)grid * block);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 4; ++r) {
+        cudaEventRecord(e0);
+        fma_peak_kernel<Real><<<grid, block>>>(out, iters, Real(1.0000001), Real(1e-9));
+        cudaEventRecord(e1);
+        e = cudaEventSynchronize(e1);
+        if (e != cudaSuccess) break;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (e != cudaSuccess) return e;
+    *tflops = 2.0 * 64 * iters * (double)grid * block / (best * 1e-3) * 1e-12;
+    return cudaGetLastError();
+}
+template cudaError_t measure_fma_peak<double>(int, double*);
+template cudaError_t measure_fma_peak<float>(int, double*);
 
 template <typename Real>
 cudaError_t launch_check_shifts(const Real* shifts, int64_t n, int* flag, cudaStream_t stream) {

@@ -205,6 +205,43 @@ __global__ void k_block_const_v(double* out, int iters, const int* __restrict__ 
     out[blockIdx.x * blockDim.x + threadIdx.x] = total;
 }
 
+// ---- 4c. every warp streams its OWN region of the constant table (what the
+// translation kernel does when warps work on different rows): TABW doubles per
+// warp, regions disjoint, each entry used once per pass.
+constexpr int TABBIG = 5200;  // 40.6 KB (the 64 KB bank also holds c_tab)
+__constant__ double c_big[TABBIG];
+template <int NO, int NI, int TL>
+__global__ void k_block_const_w(double* out, int iters, int tabw) {
+    double x[NI][TL], acc[NO][TL];
+#pragma unroll
+    for (int k = 0; k < NI; ++k)
+#pragma unroll
+        for (int t = 0; t < TL; ++t) x[k][t] = threadIdx.x * 0.001 + k + t;
+    double total = 0;
+    constexpr int BLK = NO * NI;
+    const int w = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const int lo = w * tabw;
+    for (int it = 0; it < iters; ++it) {
+        for (int base = lo; base + BLK <= lo + tabw; base += BLK) {
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+#pragma unroll
+                for (int t = 0; t < TL; ++t) acc[i][t] = 0;
+#pragma unroll
+            for (int e = 0; e < BLK; ++e) {
+                const double a = c_big[base + e];
+#pragma unroll
+                for (int t = 0; t < TL; ++t) acc[e % NO][t] = fma(a, x[e / NO][t], acc[e % NO][t]);
+            }
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+#pragma unroll
+                for (int t = 0; t < TL; ++t) total += acc[i][t];
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = total;
+}
+
 // ---- 5. shared-memory data traffic: per-lane LDS.64/STS.64 on a [q][32] column
 __global__ void k_lds_stream(double* out, int iters) {
     extern __shared__ double buf[];
@@ -346,9 +383,23 @@ int main(int argc, char** argv) {
                    "\"ms\": %.3f, \"tflops\": %.2f}\n", warps, ms, fl / ms * 1e-9);
         }
     }
+    {
+        std::vector<double> big(TABBIG);
+        for (int i = 0; i < TABBIG; ++i) big[i] = 1.0 / (1 + i % 17) - 0.3;
+        CK(cudaMemcpyToSymbol(c_big, big.data(), sizeof(double) * TABBIG));
+        for (int tabw : {100, 200, 300, 400}) {
+            const int warps = 12, block = warps * 32, grid = sms, iters = 256 * 100 / tabw;
+            float ms = time_ms([&] { k_block_const_w<10, 10, 2><<<grid, block>>>(out, iters, tabw); });
+            double fl = 2.0 * 100 * 2 * (tabw / 100) * (double)iters * grid * block;
+            printf("{\"test\": \"block_const_per_warp_region\", \"warps_per_sm\": %d, \"doubles_per_warp\": %d, "
+                   "\"working_set_kb\": %.1f, \"ms\": %.3f, \"tflops\": %.2f}\n",
+                   warps, tabw, warps * tabw * 8 / 1024.0, ms, fl / ms * 1e-9);
+        }
+    }
     for (int warps : {4, 8, 16}) {
         const int block = warps * 32, grid = sms, iters = 2000;
         const size_t smem = (size_t)warps * 64 * 32 * 8;
+        if (smem > 200 * 1024) continue;
         CK(cudaFuncSetAttribute(k_lds_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         float ms = time_ms([&] { k_lds_stream<<<grid, block, smem>>>(out, iters); });
         double bytes = 8.0 * 64 * iters * (double)grid * block;
