@@ -95,7 +95,7 @@ __device__ void swap_half_task(const HalfTaskCtx<Real>& c, int n, int cls) {
         for (int i = 0; i < nC; ++i) {
             Real acc = Real(0);
             for (int k = 0; k < nk; ++k)
-                acc = fma_(__ldg(A + k * nC + i), gather_re(c, n, cF + 2 * k), acc);
+                acc = fma_(__ldg(A + k * dF1.ld + i), gather_re(c, n, cF + 2 * k), acc);
             ure[i * kLanes] = acc;
         }
     }
@@ -105,7 +105,7 @@ __device__ void swap_half_task(const HalfTaskCtx<Real>& c, int n, int cls) {
         for (int i = 0; i < nC; ++i) {
             Real acc = Real(0);
             for (int k = 0; k < nk; ++k)
-                acc = fma_(__ldg(A + k * nC + i), gather_im(c, n, cG + 2 * k), acc);
+                acc = fma_(__ldg(A + k * dG1.ld + i), gather_im(c, n, cG + 2 * k), acc);
             uim[i * kLanes] = acc;
         }
     }
@@ -125,7 +125,7 @@ __device__ void swap_half_task(const HalfTaskCtx<Real>& c, int n, int cls) {
         const int nr = d.nrows;
         for (int i = 0; i < nr; ++i) {
             Real acc = Real(0);
-            for (int k = 0; k < nC; ++k) acc = fma_(__ldg(A + k * nr + i), ure[k * kLanes], acc);
+            for (int k = 0; k < nC; ++k) acc = fma_(__ldg(A + k * d.ld + i), ure[k * kLanes], acc);
             const int m = cF + 2 * i;
             if (c.local_side && m == 0) acc *= Real(2);
             c.buf[q_re(n, m) * kLanes] = acc;
@@ -139,7 +139,7 @@ __device__ void swap_half_task(const HalfTaskCtx<Real>& c, int n, int cls) {
             const int m = cG + 2 * i;
             if (m == 0) continue;  // Im(C_n^0) is structurally zero
             Real acc = Real(0);
-            for (int k = 0; k < nC; ++k) acc = fma_(__ldg(A + k * nr + i), uim[k * kLanes], acc);
+            for (int k = 0; k < nC; ++k) acc = fma_(__ldg(A + k * d.ld + i), uim[k * kLanes], acc);
             c.buf[q_im(n, m) * kLanes] = acc;
         }
     }

@@ -2,25 +2,26 @@
 // sfmm_tiled_f32.cu with
 //     SFMM_REAL   double | float
 //     SFMM_PMAX   largest max(p_in, p_out) this instantiation covers
-// Each including TU gets its own 64 KB constant bank for the operator tables.
 //
 // Design:
 //  * one CTA per group of 32*TL translations; lane l owns translations l and
-//    l+32 (TL = 2) so that every operator entry fetched is used by two
-//    independent FMA chains per lane;
-//  * the coefficient triangle of the whole group lives in shared memory in
-//    the compact layout buf[q][32*TL] (q = n^2 + ..., kernel_generic.cuh), every
-//    access is a unit-stride, conflict-free 64-bit access;
-//  * the swap matrices and faculty tables are read from the CONSTANT bank
-//    (LDC.64 with warp-uniform addresses feeding DFMA directly): measured
-//    29-30 TFLOP/s of 34 peak for this access pattern, against 26 TFLOP/s for
-//    shared-memory broadcast, and it leaves shared memory to the data
-//    (tools/microbench.cu, profiles/microbench_r01.jsonl);
-//  * the axis-swap pass on row n is split into its two parity halves
-//    (tables.hpp); each half is register resident: the first product runs with
-//    the class-size unrolled accumulators and a runtime loop over inputs, the
-//    second with unrolled inputs and a runtime loop over outputs, so the code
-//    size depends on the class size only (<= PMAX/2 instantiations);
+//    l+32 (TL = 2), so every operator entry fetched feeds two independent FMA
+//    chains per lane;
+//  * the coefficient triangle of the whole group lives in shared memory in a
+//    compact layout buf[q][32*TL]; every access is unit stride and conflict free;
+//  * the swap-matrix stream of the side in use (multipole: F, G; local: F^T,
+//    G^T; tables.hpp "parity blocks") is staged into shared memory with one TMA
+//    bulk copy (cp.async.bulk + mbarrier) per phase, issued while the previous
+//    phase still computes, and consumed by warp-uniform 128-bit shared loads
+//    (two entries per load). The constant bank was measured and rejected for
+//    this: it only sustains the FMA rate when all warps read the same lines
+//    (profiles/microbench_r01.jsonl: 29 TFLOP/s in lockstep, 5.5 TFLOP/s with
+//    per-warp regions; shared-memory broadcast 26 TFLOP/s regardless);
+//  * the axis-swap pass on row n is split into its two parity halves; each half
+//    is register-resident straight-line code in the class size NC only;
+//  * the z-axis step reads its Hankel/Toeplitz operator (faculties) from the
+//    constant bank through a sliding register window (all warps walk the same
+//    40-entry table, the case in which the constant path is at full speed);
 //  * arithmetic order is the reference's: k-ascending fma chains from +0.
 
 #include <algorithm>
@@ -38,46 +39,78 @@ namespace {
 using Real = SFMM_REAL;
 constexpr int PMAX = SFMM_PMAX;
 constexpr int NCMAX = PMAX / 2 + (PMAX & 1);  // largest parity-class size, rows n < PMAX
-
-constexpr int swap_stream_len(int order) {
-    int len = 0;
-    for (int n = 0; n < order; ++n) {
-        const int e = n / 2 + 1, o = (n + 1) / 2;
-        // F: (E x cF) and (O x cF'), G likewise; every block padded to even
-        const int cls[2] = {e, o};
-        for (int which = 0; which < 2; ++which)
-            for (int rc = 0; rc < 2; ++rc) {
-                const int cc = ((n + which) - rc) & 1;
-                const int sz = cls[rc] * cls[cc];
-                len += sz + (sz & 1);
-            }
-    }
-    return len;
-}
-constexpr int SWAP_LEN = swap_stream_len(PMAX);
-constexpr int SWAP_PAD = 4 * PMAX;               // tail reads of the 4-wide output tile
-constexpr int ZSEG = 2 * PMAX + 8;               // one z-table segment
+constexpr int TAB_PAD = 64;                    // finite slack behind the staged stream prefix
+constexpr int ZSEG = 2 * PMAX + 8;             // one z-table segment
 constexpr int Z_FAC = 0, Z_LOW = ZSEG, Z_UP = 2 * ZSEG;
 
-// [0, SWAP_LEN): column-major blocks; [SWAP_LEN + SWAP_PAD, ...): row-major blocks
-__constant__ Real c_sw[2 * (SWAP_LEN + SWAP_PAD)];
+template <typename T> struct vec2_of;
+template <> struct vec2_of<double> { using type = double2; };
+template <> struct vec2_of<float> { using type = float2; };
+using Vec2 = vec2_of<Real>::type;
+
+// block offsets into the parity-block stream, [n*4 + {F/E, F/O, G/E, G/O}] (same for both sides)
 __constant__ int c_blk[PMAX * 4];
 // fac[k] | lower Toeplitz (-1)^d/d! at [PMAX + d], 0 for d < 0 | upper 1/(-d)! at [PMAX + d], 0 for d > 0
 __constant__ Real c_z[3 * ZSEG];
-constexpr int RM_BASE = SWAP_LEN + SWAP_PAD;
 
 __device__ __forceinline__ int class_size(int n, int cls) { return cls ? (n + 1) >> 1 : (n >> 1) + 1; }
 
-// Shared-memory triangle of the tiled kernel: row n starts at n^2 and holds
-// re_l at 2l and im_l (l >= 1) at 2l-1, so both parts of a parity class are
-// reached from one base with compile-time strides.
+// Shared-memory triangle: row n starts at n^2 and holds re_l at 2l and
+// im_l (l >= 1) at 2l-1, so both parts of a parity class are reached from one
+// base with compile-time strides.
 __device__ __forceinline__ int t_re(int n, int l) { return n * n + 2 * l; }
 __device__ __forceinline__ int t_im(int n, int l) { return n * n + 2 * l - 1; }
 
+// ---- TMA bulk copy + mbarrier (PTX ISA: cp.async.bulk, mbarrier) -----------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                          uint64_t* bar) {
+    // the generic-proxy reads of the previous table must be ordered before the
+    // async-proxy overwrite
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, bytes);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Dynamic shared memory of the kernel. Device functions re-derive their
+// pointers from this symbol (offsets travel in Ctx) so that ptxas emits
+// LDS/STS rather than generic loads across the out-of-line calls.
+extern __shared__ __align__(16) unsigned char smem_raw[];
+
 template <int TL>
 struct Ctx {
-    Real* buf;       // lane offset applied; element q, slot t at buf[q * L + 32 t]
-    const Real* cb;  // lane offset applied; cb[m * L + 32 t]
+    int buf_off;      // element offset of the triangle buffer in smem_raw (lane not applied)
+    int tab_off;      // element offset of the staged parity-block stream
+    const Real* cb;   // global scratch, lane offset applied; cb[m * L + 32 t]
     const Real* sb;
     bool local_side, negate_sb, with_signs;
 };
@@ -85,222 +118,89 @@ struct Ctx {
 // One parity half of swap -> rotate(+-beta) -> swap on row n (reference
 // pipeline.cpp:118-136 with :155-157 / :247-249), in place in shared memory.
 //
-// For the intermediate class `cls` of size NC the real-part blocks are always
-// NC x NC; the imaginary-part blocks are NC x nG and nG x NC with
-// nG = NC-1, NC or NC+1, of which NC-1 or NC indices are usable (l = 0 carries
-// no imaginary part). Everything is straight-line code in NC so that ptxas can
-// hoist the constant-bank and shared-memory loads ahead of the FMA chains.
+// NC is the size of the intermediate class `cls`. The code is kept small on
+// purpose (one out-of-line copy per NC, shared by the forward and the backward
+// pass): with fully unrolled products the kernel was instruction-fetch bound
+// (profiles/ncu_r01_notes.md).
+//   first products:  runtime loop over the inputs k (read from shared memory),
+//                    the NC accumulators of u_re and u_im unrolled;
+//   second products: runtime loop over output rows, four per trip, the NC
+//                    inputs u[k] unrolled; a 128-bit load fetches the entries
+//                    of two adjacent rows.
+// mmax < n only for backward rows with p_out > p_in (inputs in columns
+// >= min(p_in, p_out) are zero, pipeline.cpp:229-246): the input loop is
+// simply shorter, which is exact.
 template <int TL, int NC>
-__device__ __forceinline__ void half_task_fast(const Ctx<TL>& c, int n, int cls) {
+__device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax) {
     constexpr int L = 32 * TL;
+    constexpr int LD = NC + (NC & 1);
     const int cF = (n - cls) & 1, cG = cF ^ 1;
-    const int nG = class_size(n, cG);
-    const int g0 = cG ? 0 : 1;  // first usable index of the imaginary class
-    const int nGe = nG - g0;    // NC-1 or NC
-    const int offF_cls = c_blk[n * 4 + cls], offG_cls = c_blk[n * 4 + 2 + cls];
-    const int offF_cF = c_blk[n * 4 + cF], offG_cG = c_blk[n * 4 + 2 + cG];
-    // index = base + k * ld + i with k the contracted index in both products
-    const int f1 = c.local_side ? RM_BASE + offF_cF : offF_cls;
-    const int g1 = (c.local_side ? RM_BASE + offG_cG : offG_cls) + g0 * NC;
-    const int f2 = c.local_side ? RM_BASE + offF_cls : offF_cF;
-    const int g2 = (c.local_side ? RM_BASE + offG_cls : offG_cG) + g0;
-    Real* row = c.buf + n * n * L;
-    Real* re_in = row + (2 * cF) * L;               // + 4k L
-    Real* im_in = row + (2 * (cG + 2 * g0) - 1) * L;  // + 4k L
-
-    Real ure[NC][TL], uim[NC][TL];
-    // ---- first product, real parts
-    {
-        Real x[NC][TL];
-#pragma unroll
-        for (int k = 0; k < NC; ++k)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) x[k][t] = re_in[4 * k * L + 32 * t];
-        if (c.local_side && cF == 0) {
-#pragma unroll
-            for (int t = 0; t < TL; ++t) x[0][t] *= Real(0.5);
-        }
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) ure[i][t] = Real(0);
-#pragma unroll
-        for (int k = 0; k < NC; ++k)
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[f1 + k * NC + i];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) ure[i][t] = fma_(a, x[k][t], ure[i][t]);
-            }
-    }
-    // ---- first product, imaginary parts (NC-1 inputs always, one more if nGe == NC)
-    {
-        Real x[NC][TL];
-#pragma unroll
-        for (int k = 0; k < NC - 1; ++k)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) x[k][t] = im_in[4 * k * L + 32 * t];
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) uim[i][t] = Real(0);
-#pragma unroll
-        for (int k = 0; k < NC - 1; ++k)
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[g1 + k * NC + i];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) uim[i][t] = fma_(a, x[k][t], uim[i][t]);
-            }
-        if (nGe == NC) {
-            constexpr int k = NC - 1;
-#pragma unroll
-            for (int t = 0; t < TL; ++t) x[k][t] = im_in[4 * k * L + 32 * t];
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[g1 + k * NC + i];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) uim[i][t] = fma_(a, x[k][t], uim[i][t]);
-            }
-        }
-    }
-    // ---- M2L backward gather signs (-1)^(n+l) (pipeline.cpp:235-239): constant
-    // over a parity class, so they are applied to the products instead of the inputs
-    if (c.with_signs) {
-        if (cls) {
-#pragma unroll
-            for (int i = 0; i < NC; ++i)
-#pragma unroll
-                for (int t = 0; t < TL; ++t) ure[i][t] = -ure[i][t];
-        } else {
-#pragma unroll
-            for (int i = 0; i < NC; ++i)
-#pragma unroll
-                for (int t = 0; t < TL; ++t) uim[i][t] = -uim[i][t];
-        }
-    }
-    // ---- rotate by +-beta (kernels.cpp:211-217)
-    {
-        const Real* cbp = c.cb + cls * L;
-        const Real* sbp = c.sb + cls * L;
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                const Real cm = cbp[2 * i * L + 32 * t];
-                Real sm = sbp[2 * i * L + 32 * t];
-                if (c.negate_sb) sm = -sm;
-                const Real a = ure[i][t], b = uim[i][t];
-                ure[i][t] = fma_(a, cm, -(b * sm));
-                uim[i][t] = fma_(a, sm, b * cm);
-            }
-    }
-    // ---- second product, real parts: outputs m' = cF + 2i
-    {
-        Real acc[NC][TL];
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) acc[i][t] = Real(0);
-#pragma unroll
-        for (int k = 0; k < NC; ++k)
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[f2 + k * NC + i];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) acc[i][t] = fma_(a, ure[k][t], acc[i][t]);
-            }
-        if (c.local_side && cF == 0) {
-#pragma unroll
-            for (int t = 0; t < TL; ++t) acc[0][t] *= Real(2);
-        }
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) re_in[4 * i * L + 32 * t] = acc[i][t];
-    }
-    // ---- second product, imaginary parts: outputs m' = cG + 2(i + g0), i < nGe
-    {
-        Real acc[NC][TL];
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) acc[i][t] = Real(0);
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-            const int b = g2 + k * nG;
-#pragma unroll
-            for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[b + i];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) acc[i][t] = fma_(a, uim[k][t], acc[i][t]);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < NC - 1; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) im_in[4 * i * L + 32 * t] = acc[i][t];
-        if (nGe == NC) {
-#pragma unroll
-            for (int t = 0; t < TL; ++t) im_in[4 * (NC - 1) * L + 32 * t] = acc[NC - 1][t];
-        }
-    }
-}
-
-// Same half task with runtime trip counts: used only for backward rows whose
-// inputs are truncated (columns >= min(p_in, p_out) are zero, reference
-// pipeline.cpp:229-246), i.e. for p_out > p_in.
-template <int TL, int NC>
-__device__ __noinline__ void half_task_slow(const Ctx<TL>& c, int n, int cls, int mmax) {
-    constexpr int L = 32 * TL;
-    const int cF = (n - cls) & 1, cG = cF ^ 1;
-    const int nF = class_size(n, cF), nG = class_size(n, cG);
-    const int offF_cls = c_blk[n * 4 + cls], offG_cls = c_blk[n * 4 + 2 + cls];
-    const int offF_cF = c_blk[n * 4 + cF], offG_cG = c_blk[n * 4 + 2 + cG];
-    const int f1 = c.local_side ? RM_BASE + offF_cF : offF_cls;
-    const int g1 = c.local_side ? RM_BASE + offG_cG : offG_cls;
-    const int f2 = c.local_side ? RM_BASE + offF_cls : offF_cF;
-    const int g2 = c.local_side ? RM_BASE + offG_cls : offG_cG;
+    const int nG = class_size(n, cG);      // the real class cF always has NC members
+    const int g0 = cG ? 0 : 1;             // class index 0 of E is l = 0: no imaginary part
+    const int kendF = mmax >= cF ? min(NC, ((mmax - cF) >> 1) + 1) : 0;
+    const int kendG = mmax >= cG ? min(nG, ((mmax - cG) >> 1) + 1) : 0;
+    Real* sm = reinterpret_cast<Real*>(smem_raw);
+    const Real* tab = sm + c.tab_off;
+    const Real* tF1 = tab + c_blk[n * 4 + cls];
+    const Real* tG1 = tab + c_blk[n * 4 + 2 + cls];
+    const Real* tF2 = tab + c_blk[n * 4 + cF];
+    const Real* tG2 = tab + c_blk[n * 4 + 2 + cG];
+    const int ldG2 = nG + (nG & 1);
+    Real* row = sm + c.buf_off + (threadIdx.x & 31) + n * n * L;
+    Real* re_io = row + (2 * cF) * L;      // class index k at + 4k L
+    Real* im_io = row + (2 * cG - 1) * L;  // class index k at + 4k L (k >= g0)
 
     Real ure[NC][TL], uim[NC][TL];
 #pragma unroll
     for (int i = 0; i < NC; ++i)
 #pragma unroll
         for (int t = 0; t < TL; ++t) ure[i][t] = uim[i][t] = Real(0);
-    {
-        const int kend = mmax >= cF ? min(nF, ((mmax - cF) >> 1) + 1) : 0;
-        for (int k = 0; k < kend; ++k) {
-            const int l = cF + 2 * k;
+
+    // ---- first products: u_re = A_F[cls, cF] re[cF],  u_im = A_G[cls, cG] im[cG]
+    const int kend = max(kendF, kendG);
+#pragma unroll 1
+    for (int k = 0; k < kend; ++k) {
+        if (k < kendF) {
             Real x[TL];
 #pragma unroll
-            for (int t = 0; t < TL; ++t) x[t] = c.buf[t_re(n, l) * L + 32 * t];
-            if (c.local_side && l == 0) {
+            for (int t = 0; t < TL; ++t) x[t] = re_io[4 * k * L + 32 * t];
+            if (c.local_side && k == 0 && cF == 0) {
 #pragma unroll
                 for (int t = 0; t < TL; ++t) x[t] *= Real(0.5);
             }
+            const Real* line = tF1 + k * LD;
 #pragma unroll
-            for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[f1 + k * NC + i];
+            for (int i2 = 0; i2 < LD / 2; ++i2) {
+                const Vec2 a = *reinterpret_cast<const Vec2*>(line + 2 * i2);
 #pragma unroll
-                for (int t = 0; t < TL; ++t) ure[i][t] = fma_(a, x[t], ure[i][t]);
+                for (int t = 0; t < TL; ++t) ure[2 * i2][t] = fma_(a.x, x[t], ure[2 * i2][t]);
+                if (2 * i2 + 1 < NC) {
+#pragma unroll
+                    for (int t = 0; t < TL; ++t)
+                        ure[2 * i2 + 1][t] = fma_(a.y, x[t], ure[2 * i2 + 1][t]);
+                }
             }
         }
-    }
-    {
-        const int kend = mmax >= cG ? min(nG, ((mmax - cG) >> 1) + 1) : 0;
-        for (int k = cG ? 0 : 1; k < kend; ++k) {
-            const int l = cG + 2 * k;
+        if (k >= g0 && k < kendG) {
             Real x[TL];
 #pragma unroll
-            for (int t = 0; t < TL; ++t) x[t] = c.buf[t_im(n, l) * L + 32 * t];
+            for (int t = 0; t < TL; ++t) x[t] = im_io[4 * k * L + 32 * t];
+            const Real* line = tG1 + k * LD;
 #pragma unroll
-            for (int i = 0; i < NC; ++i) {
-                const Real a = c_sw[g1 + k * NC + i];
+            for (int i2 = 0; i2 < LD / 2; ++i2) {
+                const Vec2 a = *reinterpret_cast<const Vec2*>(line + 2 * i2);
 #pragma unroll
-                for (int t = 0; t < TL; ++t) uim[i][t] = fma_(a, x[t], uim[i][t]);
+                for (int t = 0; t < TL; ++t) uim[2 * i2][t] = fma_(a.x, x[t], uim[2 * i2][t]);
+                if (2 * i2 + 1 < NC) {
+#pragma unroll
+                    for (int t = 0; t < TL; ++t)
+                        uim[2 * i2 + 1][t] = fma_(a.y, x[t], uim[2 * i2 + 1][t]);
+                }
             }
         }
     }
+    // M2L backward gather signs (-1)^(n+l) (pipeline.cpp:235-239) are constant over a
+    // parity class: applied to the products instead of the inputs (exact)
     if (c.with_signs) {
 #pragma unroll
         for (int i = 0; i < NC; ++i)
@@ -310,64 +210,96 @@ __device__ __noinline__ void half_task_slow(const Ctx<TL>& c, int n, int cls, in
                 else uim[i][t] = -uim[i][t];
             }
     }
+    // ---- rotate by +-beta (kernels.cpp:211-217); factors from the global scratch
+    {
+        const Real* cbp = c.cb + cls * L;
+        const Real* sbp = c.sb + cls * L;
+        Real cm[NC][TL], sn[NC][TL];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
-        const int m = cls + 2 * i;
+        for (int i = 0; i < NC; ++i)
 #pragma unroll
-        for (int t = 0; t < TL; ++t) {
-            const Real cm = c.cb[m * L + 32 * t];
-            Real sm = c.sb[m * L + 32 * t];
-            if (c.negate_sb) sm = -sm;
-            const Real a = ure[i][t], b = uim[i][t];
-            ure[i][t] = fma_(a, cm, -(b * sm));
-            uim[i][t] = fma_(a, sm, b * cm);
-        }
+            for (int t = 0; t < TL; ++t) {
+                cm[i][t] = __ldcg(cbp + 2 * i * L + 32 * t);
+                sn[i][t] = __ldcg(sbp + 2 * i * L + 32 * t);
+            }
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                const Real s = c.negate_sb ? -sn[i][t] : sn[i][t];
+                const Real a = ure[i][t], b = uim[i][t];
+                ure[i][t] = fma_(a, cm[i][t], -(b * s));
+                uim[i][t] = fma_(a, s, b * cm[i][t]);
+            }
     }
-    for (int i = 0; i < nF; ++i) {
-        Real acc[TL];
+    // ---- second products: re[cF] = A_F[cF, cls] u_re,  im[cG] = A_G[cG, cls] u_im.
+    // Output class index r (m' = class + 2r), rows r .. r+3 per trip.
+#pragma unroll 1
+    for (int r = 0; r < NC; r += 4) {
+        Real acc[4][TL];
 #pragma unroll
-        for (int t = 0; t < TL; ++t) acc[t] = Real(0);
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) acc[j][t] = Real(0);
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
-            const Real a = c_sw[f2 + k * nF + i];
+            const Vec2 a0 = *reinterpret_cast<const Vec2*>(tF2 + k * LD + r);
+            const Vec2 a1 = *reinterpret_cast<const Vec2*>(tF2 + k * LD + r + 2);
 #pragma unroll
-            for (int t = 0; t < TL; ++t) acc[t] = fma_(a, ure[k][t], acc[t]);
+            for (int t = 0; t < TL; ++t) {
+                acc[0][t] = fma_(a0.x, ure[k][t], acc[0][t]);
+                acc[1][t] = fma_(a0.y, ure[k][t], acc[1][t]);
+                acc[2][t] = fma_(a1.x, ure[k][t], acc[2][t]);
+                acc[3][t] = fma_(a1.y, ure[k][t], acc[3][t]);
+            }
         }
-        const int m = cF + 2 * i;
+        if (c.local_side && r == 0 && cF == 0) {
 #pragma unroll
-        for (int t = 0; t < TL; ++t) {
-            Real v = acc[t];
-            if (c.local_side && m == 0) v *= Real(2);
-            c.buf[t_re(n, m) * L + 32 * t] = v;
+            for (int t = 0; t < TL; ++t) acc[0][t] *= Real(2);
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (r + j < NC) {
+#pragma unroll
+                for (int t = 0; t < TL; ++t) re_io[4 * (r + j) * L + 32 * t] = acc[j][t];
+            }
     }
-    for (int i = cG ? 0 : 1; i < nG; ++i) {
-        Real acc[TL];
+#pragma unroll 1
+    for (int r = 0; r < nG; r += 4) {
+        Real acc[4][TL];
 #pragma unroll
-        for (int t = 0; t < TL; ++t) acc[t] = Real(0);
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) acc[j][t] = Real(0);
+        const Real* base = tG2 + r;
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
-            const Real a = c_sw[g2 + k * nG + i];
+            const Vec2 a0 = *reinterpret_cast<const Vec2*>(base + k * ldG2);
+            const Vec2 a1 = *reinterpret_cast<const Vec2*>(base + k * ldG2 + 2);
 #pragma unroll
-            for (int t = 0; t < TL; ++t) acc[t] = fma_(a, uim[k][t], acc[t]);
+            for (int t = 0; t < TL; ++t) {
+                acc[0][t] = fma_(a0.x, uim[k][t], acc[0][t]);
+                acc[1][t] = fma_(a0.y, uim[k][t], acc[1][t]);
+                acc[2][t] = fma_(a1.x, uim[k][t], acc[2][t]);
+                acc[3][t] = fma_(a1.y, uim[k][t], acc[3][t]);
+            }
         }
-        const int m = cG + 2 * i;
 #pragma unroll
-        for (int t = 0; t < TL; ++t) c.buf[t_im(n, m) * L + 32 * t] = acc[t];
+        for (int j = 0; j < 4; ++j)
+            if (r + j < nG && r + j >= g0) {
+#pragma unroll
+                for (int t = 0; t < TL; ++t) im_io[4 * (r + j) * L + 32 * t] = acc[j][t];
+            }
     }
 }
 
 template <int TL>
-__device__ __forceinline__ void half_task_dispatch(const Ctx<TL>& c, int n, int cls, int mmax) {
+__device__ __forceinline__ void half_task_dispatch(const Ctx<TL> c, int n, int cls, int mmax) {
     const int nc = class_size(n, cls);
-    const bool full = mmax >= n;
     switch (nc) {
-#define SFMM_CASE(K)                                        \
-    case K:                                                 \
-        if constexpr (K <= NCMAX) {                         \
-            if (full) half_task_fast<TL, K>(c, n, cls);     \
-            else half_task_slow<TL, K>(c, n, cls, mmax);    \
-        }                                                   \
+#define SFMM_CASE(K)                                             \
+    case K:                                                      \
+        if constexpr (K <= NCMAX) half_task<TL, K>(c, n, cls, mmax); \
         break;
         SFMM_CASE(1) SFMM_CASE(2) SFMM_CASE(3) SFMM_CASE(4) SFMM_CASE(5)
         SFMM_CASE(6) SFMM_CASE(7) SFMM_CASE(8) SFMM_CASE(9) SFMM_CASE(10)
@@ -380,10 +312,10 @@ __device__ __forceinline__ void half_task_dispatch(const Ctx<TL>& c, int n, int 
 // (reference kernels.cpp:118-196). The operator is Hankel (M2L: (2m+i+k)!) or
 // Toeplitz (M2M/L2L), so four k-steps share one sliding window of R+3 entries.
 template <int TL, int R, int DIR>
-__device__ __forceinline__ void zstep_task(Real* buf, int zi, int p_in, int p_out, int m,
-                                           int part) {
+__device__ __noinline__ void zstep_task(int buf_off, int zi, int p_in, int p_out, int m, int part) {
     constexpr int L = 32 * TL;
     const int kin = p_in - m, kout = p_out - m;
+    Real* buf = reinterpret_cast<Real*>(smem_raw) + buf_off + (threadIdx.x & 31);
     Real* col = buf + (part ? t_im(m, m) : t_re(m, m)) * L;  // element k at col[(2 m k + k^2) L]
     Real acc[R][TL];
 #pragma unroll
@@ -432,7 +364,7 @@ __device__ __forceinline__ void zstep_task(Real* buf, int zi, int p_in, int p_ou
 }
 
 template <int TL>
-__device__ __forceinline__ void zstep_dispatch(Real* buf, int kind, int p_in, int p_out, int m,
+__device__ __forceinline__ void zstep_dispatch(int buf, int kind, int p_in, int p_out, int m,
                                                int part) {
     const int r4 = (p_out - m + 3) >> 2;
     const int zi = kind == KIND_M2L ? Z_FAC + 2 * m : (kind == KIND_M2M ? Z_LOW + PMAX : Z_UP + PMAX);
@@ -460,10 +392,11 @@ template <int TL>
 struct TiledLayout {
     static constexpr int L = 32 * TL;
     int p_rot;
+    size_t tab_len;  // staged stream elements (prefix + TAB_PAD, multiple of 4)
     __host__ __device__ size_t buf_elems() const { return (size_t)p_rot * p_rot * L; }
-    __host__ __device__ size_t tab_elems() const { return (size_t)(2 * p_rot + 4) * L; }
+    __host__ __device__ size_t geo_elems() const { return (size_t)4 * L; }
     __host__ __device__ size_t smem_bytes() const {
-        return sizeof(Real) * (buf_elems() + tab_elems()) + 16;
+        return sizeof(Real) * (buf_elems() + tab_len + geo_elems()) + 32;
     }
 };
 
@@ -479,32 +412,59 @@ struct TriWalk {
     }
 };
 
+struct TiledTables {
+    const Real* stream[2];  // global parity-block streams: [0] multipole side, [1] local side
+    uint32_t bytes[2];      // bytes staged for the forward / backward pass
+    Real* beta;             // global scratch: per CTA cb[p_rot][L], sb[p_rot][L]
+};
+
 template <int TL>
-__global__ void __launch_bounds__(384, 1)
-translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
+__global__ void __launch_bounds__(256, 1)
+translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, int p_rot,
+                       int tab_len) {
     constexpr int L = 32 * TL;
     constexpr int CH = 4;  // elements whose global loads are issued together
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     if (a.fail_flag && *a.fail_flag) return;
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int W = blockDim.x >> 5;
-    const TiledLayout<TL> lay{p_rot};
+    const TiledLayout<TL> lay{p_rot, (size_t)tab_len};
 
     Real* sm = reinterpret_cast<Real*>(smem_raw);
-    Real* buf = sm + lane;
-    Real* cb = sm + lay.buf_elems() + lane;
-    Real* sb = cb + (size_t)p_rot * L;
-    Real* geo = sb + (size_t)p_rot * L;  // ca1, sa1, rn, 1/rn
-    int* counters = reinterpret_cast<int*>(sm + lay.buf_elems() + lay.tab_elems());
+    Real* tab = sm;  // 16-byte aligned
+    Real* buf = sm + lay.tab_len + lane;
+    Real* geo = sm + lay.tab_len + lay.buf_elems() + lane;  // ca1, sa1, rn, 1/rn
+    uint64_t* mbar =
+        reinterpret_cast<uint64_t*>(sm + lay.tab_len + lay.buf_elems() + lay.geo_elems());
+    int* counters = reinterpret_cast<int*>(mbar + 1);
+    Real* cbg = tt.beta + (size_t)blockIdx.x * 2 * p_rot * L + lane;
+    Real* sbg = cbg + (size_t)p_rot * L;
 
     const int kind = a.kind, p_in = a.p_in, p_out = a.p_out;
     const bool src_local = kind == KIND_L2L;
     const bool dst_local = kind != KIND_M2M;
+    const int side_fwd = src_local ? 1 : 0, side_bwd = dst_local ? 1 : 0;
+    const bool two_sides = side_fwd != side_bwd;
     const int cols = min(p_in, p_out);
     const bool accumulate = a.src_index != nullptr;
 
+    // table staging: one mbarrier, completions alternate fwd / bwd tables
+    uint32_t tab_phase = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        bulk_load(tab, tt.stream[side_fwd], two_sides ? tt.bytes[0] : max(tt.bytes[0], tt.bytes[1]),
+                  mbar);
+    }
+    bool tab_pending = true;  // a bulk copy is in flight that the next swap phase must wait for
+
+    long long t_prev = clock64();
+#define SFMM_PHASE_MARK(idx)                                              \
+    if (a.phase_clocks && blockIdx.x == 0 && threadIdx.x == 0) {          \
+        const long long now = clock64();                                  \
+        a.phase_clocks[idx] += now - t_prev;                              \
+        t_prev = now;                                                     \
+    }
     for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
         int64_t b[TL], src[TL];
         bool active[TL];
@@ -538,8 +498,8 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
                 geo[3 * L + 32 * t] = Real(1) / ang.rn;
                 Real c = 1, s = 0;
                 for (int m = 0; m < p_rot; ++m) {
-                    cb[m * L + 32 * t] = c;
-                    sb[m * L + 32 * t] = s;
+                    cbg[m * L + 32 * t] = c;
+                    sbg[m * L + 32 * t] = s;
                     const Real nc = fma_(c, ang.cb, -(s * ang.sb));
                     const Real ns = fma_(s, ang.cb, c * ang.sb);
                     c = nc;
@@ -549,6 +509,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
         }
         if (threadIdx.x == 0) counters[0] = counters[1] = counters[2] = 0;
         __syncthreads();
+        SFMM_PHASE_MARK(0)
 
         // ---- A: load, rotate by +alpha, scale (pipeline.cpp:148-154); each warp
         // takes an equal share of the column-major element list
@@ -597,7 +558,8 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
 #pragma unroll
                         for (int t = 0; t < TL; ++t) {
                             re[u][t] = active[t] ? a.in[off + src[t]] : Real(0);
-                            im[u][t] = (active[t] && wl.m) ? a.in[off + a.in_stride + src[t]] : Real(0);
+                            im[u][t] =
+                                (active[t] && wl.m) ? a.in[off + a.in_stride + src[t]] : Real(0);
                         }
                         wl.advance();
                     }
@@ -631,11 +593,17 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
                 e += cnt;
             }
         }
+        if (tab_pending) {
+            mbar_wait(mbar, tab_phase);
+            tab_phase ^= 1;
+            tab_pending = false;
+        }
         __syncthreads();
+        SFMM_PHASE_MARK(1)
 
         // ---- B: forward swap passes, largest rows first
         {
-            Ctx<TL> c{buf, cb, sb, src_local, false, false};
+            Ctx<TL> c{(int)lay.tab_len, 0, cbg, sbg, src_local, false, false};
             for (int task = fetch_task(&counters[0], lane); task < 2 * p_in;
                  task = fetch_task(&counters[0], lane)) {
                 const int n = p_in - 1 - (task >> 1);
@@ -643,20 +611,31 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
             }
         }
         __syncthreads();
+        SFMM_PHASE_MARK(2)
+        if (two_sides) {  // stage the backward-side stream while the z-step runs
+            if (threadIdx.x == 0) bulk_load(tab, tt.stream[side_bwd], tt.bytes[1], mbar);
+            tab_pending = true;
+        }
 
         // ---- Z: z-axis step per (column, re|im), longest columns first
         for (int task = fetch_task(&counters[1], lane); task < 2 * cols;
              task = fetch_task(&counters[1], lane)) {
             const int m = task >> 1, part = task & 1;
             if (part && m == 0) continue;
-            zstep_dispatch<TL>(buf, kind, p_in, p_out, m, part);
+            zstep_dispatch<TL>((int)lay.tab_len, kind, p_in, p_out, m, part);
+        }
+        if (tab_pending) {
+            mbar_wait(mbar, tab_phase);
+            tab_phase ^= 1;
+            tab_pending = false;
         }
         __syncthreads();
+        SFMM_PHASE_MARK(3)
 
         // ---- C: backward swap passes; columns >= cols of the z-step output are
         // zero (pipeline.cpp:229-246) and are skipped, which is exact
         {
-            Ctx<TL> c{buf, cb, sb, dst_local, true, kind == KIND_M2L};
+            Ctx<TL> c{(int)lay.tab_len, 0, cbg, sbg, dst_local, true, kind == KIND_M2L};
             for (int task = fetch_task(&counters[2], lane); task < 2 * p_out;
                  task = fetch_task(&counters[2], lane)) {
                 const int n = p_out - 1 - (task >> 1);
@@ -664,6 +643,11 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
             }
         }
         __syncthreads();
+        SFMM_PHASE_MARK(4)
+        if (two_sides && g + gridDim.x < n_groups) {  // forward-side stream for the next group
+            if (threadIdx.x == 0) bulk_load(tab, tt.stream[side_fwd], tt.bytes[0], mbar);
+            tab_pending = true;
+        }
 
         // ---- D: rotate by -alpha, scale (pipeline.cpp:251-257), store or reduce
         {
@@ -749,37 +733,25 @@ translate_tiled_kernel(TranslateArgs<Real> a, int64_t n_groups, int p_rot) {
             }
         }
         __syncthreads();
+        SFMM_PHASE_MARK(5)
     }
+#undef SFMM_PHASE_MARK
 }
 
 // ---- host side: constant-bank upload (once per device and process) --------
 
 struct HostTables {
-    std::vector<Real> sw;
     std::vector<int> blk;
     std::vector<Real> z;
-    bool ok = false;
 };
 
 HostTables build_host_tables() {
     HostTables h;
     const SwapTables st(PMAX);
-    const PackedSide cm = pack_side(st, false);  // column-major blocks of F, G
-    if ((int)cm.stream.size() != SWAP_LEN) return h;  // constexpr layout out of sync with tables.cpp
-    h.ok = true;
-    h.sw.assign(2 * (SWAP_LEN + SWAP_PAD), Real(0));
+    const PackedSide ps = pack_side(st, false);
     h.blk.assign(PMAX * 4, 0);
     for (int n = 0; n < PMAX; ++n)
-        for (int j = 0; j < 4; ++j) {
-            const BlockDesc& d = cm.desc[(size_t)n * 4 + j];
-            h.blk[n * 4 + j] = (int)d.offset;
-            for (int k = 0; k < d.ncols; ++k)
-                for (int i = 0; i < d.nrows; ++i) {
-                    const Real v = static_cast<Real>(cm.stream[d.offset + (size_t)k * d.nrows + i]);
-                    h.sw[d.offset + (size_t)k * d.nrows + i] = v;            // column-major
-                    h.sw[RM_BASE + d.offset + (size_t)i * d.ncols + k] = v;  // row-major
-                }
-        }
+        for (int j = 0; j < 4; ++j) h.blk[n * 4 + j] = (int)ps.desc[(size_t)n * 4 + j].offset;
     std::vector<Real> fac, inv;
     build_faculties<Real>(PMAX, fac, inv);
     h.z.assign(3 * ZSEG, Real(0));
@@ -801,9 +773,6 @@ cudaError_t ensure_constants() {
     for (int d : done)
         if (d == dev) return cudaSuccess;
     static const HostTables h = build_host_tables();
-    if (!h.ok) return cudaErrorInvalidValue;
-    e = cudaMemcpyToSymbol(c_sw, h.sw.data(), sizeof(Real) * h.sw.size());
-    if (e != cudaSuccess) return e;
     e = cudaMemcpyToSymbol(c_blk, h.blk.data(), sizeof(int) * h.blk.size());
     if (e != cudaSuccess) return e;
     e = cudaMemcpyToSymbol(c_z, h.z.data(), sizeof(Real) * h.z.size());
@@ -815,10 +784,9 @@ cudaError_t ensure_constants() {
 int tiled_warps_for(int p_rot) {
     if (const char* env = getenv("SFMM_TILED_WARPS")) {
         const int w = atoi(env);
-        if (w >= 2 && w <= 12) return w;
+        if (w >= 2 && w <= 8) return w;
     }
-    if (p_rot >= 14) return 12;
-    if (p_rot >= 8) return 8;
+    if (p_rot >= 12) return 8;
     return 4;
 }
 
@@ -828,15 +796,23 @@ bool tiled_supports(const TranslateArgs<Real>& a) {
     return std::max(a.p_in, a.p_out) <= PMAX;
 }
 
-cudaError_t launch_translate_tiled(const TranslateArgs<Real>& a, int sm_count,
-                                   cudaStream_t stream, LaunchInfo* info) {
+cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateArgs<Real>& a,
+                                   int sm_count, cudaStream_t stream, LaunchInfo* info) {
     constexpr int TL = 2;
+    constexpr int L = 32 * TL;
     cudaError_t e = ensure_constants();
     if (e != cudaSuccess) return e;
     const int p_rot = std::max(a.p_in, a.p_out);
-    const TiledLayout<TL> lay{p_rot};
+    // the staged prefix plus a finite pad (tail reads of dropped rows), in 16-byte units
+    auto staged = [&](int p) {
+        size_t len = packed_prefix_len(p) + TAB_PAD;
+        return (len + 3) / 4 * 4;
+    };
+    const size_t tab_len = std::max(staged(a.p_in), staged(a.p_out));
+    if (tab_len > t.stream_len[0] || tab_len > t.stream_len[1]) return cudaErrorInvalidValue;
+    const TiledLayout<TL> lay{p_rot, tab_len};
     const size_t smem = lay.smem_bytes();
-    const int64_t n_groups = (a.n + 32 * TL - 1) / (32 * TL);
+    const int64_t n_groups = (a.n + L - 1) / L;
     const int block = 32 * tiled_warps_for(p_rot);
     auto kern = translate_tiled_kernel<TL>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -846,7 +822,17 @@ cudaError_t launch_translate_tiled(const TranslateArgs<Real>& a, int sm_count,
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     const int grid = (int)std::min<int64_t>(n_groups, (int64_t)sm_count * per_sm);
-    kern<<<grid, block, smem, stream>>>(a, n_groups, p_rot);
+
+    TiledTables tt;
+    tt.stream[0] = t.stream[0];
+    tt.stream[1] = t.stream[1];
+    tt.bytes[0] = (uint32_t)(staged(a.p_in) * sizeof(Real));
+    tt.bytes[1] = (uint32_t)(staged(a.p_out) * sizeof(Real));
+    e = cudaMallocAsync((void**)&tt.beta, sizeof(Real) * (size_t)grid * 2 * p_rot * L, stream);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, block, smem, stream>>>(a, tt, n_groups, p_rot, (int)tab_len);
+    e = cudaGetLastError();
+    cudaFreeAsync(tt.beta, stream);
     if (info) {
         info->grid = grid;
         info->block = block;
@@ -854,7 +840,7 @@ cudaError_t launch_translate_tiled(const TranslateArgs<Real>& a, int sm_count,
         info->launches = 1;
         info->variant = sizeof(Real) == 8 ? "tiled/f64/TL2" : "tiled/f32/TL2";
     }
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace sfmm

@@ -69,6 +69,7 @@ struct sfmm_handle {
     std::mutex async_mutex;
     std::vector<int> async_slots;
     int variant = 0;
+    long long* d_phase_clocks = nullptr;  // set by the "phase_clocks" option
 };
 
 struct sfmm_plan {
@@ -86,8 +87,10 @@ sfmm_status upload_tables(sfmm_handle* h, DeviceTables<Real>& t) {
     t.order = h->order;
     for (int side = 0; side < 2; ++side) {
         const PackedSide ps = pack_side(h->host_tables, side == 1);
-        std::vector<Real> s(ps.stream.size());
-        for (size_t i = 0; i < s.size(); ++i) s[i] = static_cast<Real>(ps.stream[i]);
+        // zero slack behind the stream: the tiled kernel stages a fixed pad past
+        // the prefix it needs (kernel_tiled.inl, TAB_PAD)
+        std::vector<Real> s(ps.stream.size() + 128, Real(0));
+        for (size_t i = 0; i < ps.stream.size(); ++i) s[i] = static_cast<Real>(ps.stream[i]);
         Real* ds = nullptr;
         BlockDesc* dd = nullptr;
         CU(cudaMalloc((void**)&ds, std::max<size_t>(s.size(), 2) * sizeof(Real)));
@@ -175,6 +178,7 @@ sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, in
     a.out_stride = out_stride;
     a.fail_flag = d_flag;
     a.variant = h->variant;
+    a.phase_clocks = h->d_phase_clocks;
     LaunchInfo info;
     CU(launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info));
     h->launches += info.launches;
@@ -343,6 +347,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.out_stride = plan->n_groups;
     a.src_index = plan->d_src_index;
     a.variant = h->variant;
+    a.phase_clocks = h->d_phase_clocks;
     LaunchInfo info;
     cudaError_t e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
     h->launches += info.launches;
@@ -489,6 +494,11 @@ sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
     if (std::strcmp(name, "kernel_variant") == 0) {
         if (value < 0 || value > 2) return fail(SFMM_INVALID_ARGUMENT, "kernel_variant must be 0, 1 or 2");
         h->variant = (int)value;
+        return SFMM_OK;
+    }
+    if (std::strcmp(name, "phase_clocks") == 0) {
+        // value = device address of 8 int64 counters (0 switches the probe off)
+        h->d_phase_clocks = reinterpret_cast<long long*>(value);
         return SFMM_OK;
     }
     return fail(SFMM_INVALID_ARGUMENT, std::string("unknown option ") + name);

@@ -39,6 +39,7 @@ struct TranslateArgs {
     const int32_t* src_index = nullptr;  // accumulate mode: source per lane, -1 = idle lane
     const int* fail_flag = nullptr;      // device int; non-zero -> kernel writes nothing
     int variant = 0;                     // 0 auto, 1 generic kernel, 2 tiled kernel
+    long long* phase_clocks = nullptr;   // optional [8] cycle counters of CTA 0 (tuning aid)
 };
 
 struct LaunchInfo {
@@ -56,10 +57,10 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
 // Tuned kernels (kernel_tiled.inl): orders <= 20 (double) / <= 18 (float).
 bool tiled_supports(const TranslateArgs<double>& a);
 bool tiled_supports(const TranslateArgs<float>& a);
-cudaError_t launch_translate_tiled(const TranslateArgs<double>& a, int sm_count,
-                                   cudaStream_t stream, LaunchInfo* info);
-cudaError_t launch_translate_tiled(const TranslateArgs<float>& a, int sm_count,
-                                   cudaStream_t stream, LaunchInfo* info);
+cudaError_t launch_translate_tiled(const DeviceTables<double>& t, const TranslateArgs<double>& a,
+                                   int sm_count, cudaStream_t stream, LaunchInfo* info);
+cudaError_t launch_translate_tiled(const DeviceTables<float>& t, const TranslateArgs<float>& a,
+                                   int sm_count, cudaStream_t stream, LaunchInfo* info);
 
 // Measured FMA-pipe peak of the current device in the given precision.
 template <typename Real>

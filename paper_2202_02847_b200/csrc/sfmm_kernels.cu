@@ -177,7 +177,7 @@ template <typename Real>
 cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Real>& a,
                              int sm_count, cudaStream_t stream, LaunchInfo* info) {
     if (a.n <= 0) return cudaSuccess;
-    if (a.variant != 1 && tiled_supports(a)) return launch_translate_tiled(a, sm_count, stream, info);
+    if (a.variant != 1 && tiled_supports(a)) return launch_translate_tiled(t, a, sm_count, stream, info);
     if (a.variant == 2) return cudaErrorInvalidValue;
     const int p_rot = std::max(a.p_in, a.p_out);
     const int64_t n_groups = (a.n + kLanes - 1) / kLanes;

@@ -112,7 +112,8 @@ PackedSide pack_side(const SwapTables& t, bool local_side) {
                 d.ncols = static_cast<uint16_t>(cls_size[cc]);
                 d.row_class = static_cast<uint8_t>(rc);
                 d.col_class = static_cast<uint8_t>(cc);
-                for (int kk = 0; kk < d.ncols; ++kk)
+                d.ld = static_cast<uint16_t>(d.nrows + (d.nrows & 1));
+                for (int kk = 0; kk < d.ncols; ++kk) {
                     for (int ii = 0; ii < d.nrows; ++ii) {
                         const int i = rc + 2 * ii, k = cc + 2 * kk;
                         const size_t idx = local_side
@@ -120,12 +121,26 @@ PackedSide pack_side(const SwapTables& t, bool local_side) {
                                                : static_cast<size_t>(i) * rows + k;
                         out.stream.push_back(a[idx]);
                     }
-                if (out.stream.size() & 1) out.stream.push_back(0.0);
+                    if (d.nrows & 1) out.stream.push_back(0.0);
+                }
                 out.desc[static_cast<size_t>(n) * 4 + which * 2 + rc] = d;
             }
         }
     }
     return out;
+}
+
+size_t packed_prefix_len(int order) {
+    size_t len = 0;
+    for (int n = 0; n < order; ++n) {
+        const int cls[2] = {n / 2 + 1, (n + 1) / 2};
+        for (int which = 0; which < 2; ++which)
+            for (int rc = 0; rc < 2; ++rc) {
+                const int cc = ((n + which) - rc) & 1;
+                len += static_cast<size_t>(cls[rc] + (cls[rc] & 1)) * cls[cc];
+            }
+    }
+    return len;
 }
 
 }  // namespace sfmm

@@ -43,16 +43,17 @@ void build_faculties(int order, std::vector<Real>& fac, std::vector<Real>& inv);
 //
 //   F rows E, F rows O, G rows E, G rows O
 //
-// each stored COLUMN-major (entry (i,k) at k*rows_in_class + i, i.e. in the
-// order a k-outer / i-inner FMA loop consumes it), padded to an even number of
-// entries so every block starts 16-byte aligned in double.
+// each stored COLUMN-major with the column ("line") padded to an even length
+// ld: entry (i,k) at k*ld + i, i.e. in the order a k-outer / i-inner FMA loop
+// consumes it, every line 16-byte aligned in double so that two entries can be
+// fetched with one 128-bit shared-memory load.
 struct BlockDesc {
     uint32_t offset;   // element offset of the block in the stream
     uint16_t nrows;    // outputs: size of the row class
     uint16_t ncols;    // inputs: size of the column class
     uint8_t row_class; // 0 even, 1 odd
     uint8_t col_class;
-    uint8_t pad[2];
+    uint16_t ld;       // padded line length (nrows rounded up to even)
 };
 
 struct PackedSide {
@@ -64,5 +65,9 @@ struct PackedSide {
 // local_side == false: A = F_n, G_n (multipole-type data);
 // local_side == true:  A = F_n^T, G_n^T (local-type data).
 PackedSide pack_side(const SwapTables& t, bool local_side);
+
+// Number of stream elements occupied by rows n < order (the stream is ordered
+// by n, so the tables of a lower order are a prefix).
+size_t packed_prefix_len(int order);
 
 }  // namespace sfmm

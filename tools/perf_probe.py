@@ -44,6 +44,11 @@ else:
     run = lambda: plan.accumulate(P, P, d_src.data_ptr(), sstride, d_out.data_ptr(), ostride, stream)
     units = int(tp[-1])
 
+import os
+pc = None
+if os.environ.get("PHASES"):
+    pc = torch.zeros(8, dtype=torch.int64, device=dev)
+    h.set_option("phase_clocks", pc.data_ptr())
 for _ in range(2): run()
 torch.cuda.synchronize()
 best = 1e9
@@ -51,6 +56,10 @@ for _ in range(reps):
     e0.record(); run(); e1.record(); torch.cuda.synchronize()
     best = min(best, e0.elapsed_time(e1))
 h.stream_status(stream)
+if pc is not None:
+    v = pc.cpu().numpy().astype(float); tot = v.sum()
+    names = ["G geometry", "A load+rot", "B fwd swaps", "Z z-step", "C bwd swaps", "D rot+store"]
+    print("phase cycles of CTA 0 (all launches):", ", ".join(f"{n}: {100*x/tot:.1f}%" for n, x in zip(names, v)), f"total {tot:.3e}")
 tps = units / (best * 1e-3)
 print(f"{mode} {kind} P={P} units={units} best_ms={best:.3f} translations/s={tps:.3e} "
       f"TFLOP/s={tps*flops*1e-12:.2f} of peak {peak:.1f} => frac={tps*flops*1e-12/peak:.3f}", flush=True)
