@@ -111,33 +111,82 @@ struct Ctx {
     int buf_off;      // element offset of the triangle buffer in smem_raw (lane not applied)
     int tab_off;      // element offset of the staged parity-block stream
     const Real* cb;   // global scratch, lane offset applied; cb[m * L + 32 t]
-    const Real* sb;
-    bool local_side, negate_sb, with_signs;
+    const Real* sb;   // sin table of the pass: +sin(m beta) forward, -sin(m beta) backward
+    bool local_side;
 };
+
+// acc[i][t] += sum_{k0 <= k < kend} line_k[i] * in[4 k L + 32 t]: lines of padded length ld
+// at tab + k ld (warp-uniform 128-bit loads, two entries each), software pipelined.
+template <int TL, int NCE>
+__device__ __forceinline__ void first_product(const Real* tab, int ld, const Real* in, int k0,
+                                              int kend, bool halve_first, Real (&acc)[NCE][TL]) {
+    constexpr int L = 32 * TL;
+    if (k0 >= kend) return;
+    Vec2 a[NCE / 2];
+    Real x[TL];
+    {
+        const Real* line = tab + k0 * ld;
+#pragma unroll
+        for (int i2 = 0; i2 < NCE / 2; ++i2) a[i2] = *reinterpret_cast<const Vec2*>(line + 2 * i2);
+#pragma unroll
+        for (int t = 0; t < TL; ++t) x[t] = in[4 * k0 * L + 32 * t];
+        if (halve_first) {
+#pragma unroll
+            for (int t = 0; t < TL; ++t) x[t] *= Real(0.5);
+        }
+    }
+#pragma unroll 2
+    for (int k = k0; k < kend; ++k) {
+        Vec2 an[NCE / 2];
+        Real xn[TL];
+        const int kn = min(k + 1, kend - 1);  // the last trip reloads its own operands
+        const Real* line = tab + kn * ld;
+#pragma unroll
+        for (int i2 = 0; i2 < NCE / 2; ++i2) an[i2] = *reinterpret_cast<const Vec2*>(line + 2 * i2);
+#pragma unroll
+        for (int t = 0; t < TL; ++t) xn[t] = in[4 * kn * L + 32 * t];
+#pragma unroll
+        for (int i2 = 0; i2 < NCE / 2; ++i2)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                acc[2 * i2][t] = fma_(a[i2].x, x[t], acc[2 * i2][t]);
+                acc[2 * i2 + 1][t] = fma_(a[i2].y, x[t], acc[2 * i2 + 1][t]);
+            }
+#pragma unroll
+        for (int i2 = 0; i2 < NCE / 2; ++i2) a[i2] = an[i2];
+#pragma unroll
+        for (int t = 0; t < TL; ++t) x[t] = xn[t];
+    }
+}
 
 // One parity half of swap -> rotate(+-beta) -> swap on row n (reference
 // pipeline.cpp:118-136 with :155-157 / :247-249), in place in shared memory.
 //
-// NC is the size of the intermediate class `cls`. The code is kept small on
-// purpose (one out-of-line copy per NC, shared by the forward and the backward
-// pass): with fully unrolled products the kernel was instruction-fetch bound
-// (profiles/ncu_r01_notes.md).
+// CODE SIZE IS A FIRST-ORDER CONSTRAINT HERE: the B200 instruction cache holds
+// about 32 KB per SM and execution slows ~5x once the code the warps of an SM
+// run concurrently exceeds it (profiles/icache_probe_r01.jsonl). The warps of
+// a CTA work on different rows at the same time, so the half task exists in
+// only four sizes NCE in {4, 6, 8, 10} (~20 KB together), each out of line and
+// shared by the forward and the backward pass; a class of nc = NCE-1 members
+// runs in the NCE code with one idle accumulator (the table lines are padded
+// to even length with zeros, so the idle lane stays exactly zero).
 //   first products:  runtime loop over the inputs k (read from shared memory),
-//                    the NC accumulators of u_re and u_im unrolled;
-//   second products: runtime loop over output rows, four per trip, the NC
-//                    inputs u[k] unrolled; a 128-bit load fetches the entries
+//                    the NCE accumulators of u_re and u_im unrolled;
+//   second products: runtime loop over output rows, four per trip, the NCE
+//                    inputs u[k] unrolled; one 128-bit load fetches the entries
 //                    of two adjacent rows.
 // mmax < n only for backward rows with p_out > p_in (inputs in columns
 // >= min(p_in, p_out) are zero, pipeline.cpp:229-246): the input loop is
 // simply shorter, which is exact.
-template <int TL, int NC>
+template <int TL, int NCE>
 __device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax) {
     constexpr int L = 32 * TL;
-    constexpr int LD = NC + (NC & 1);
+    const int nc = class_size(n, cls);     // 1 <= nc <= NCE
+    const int ld = nc + (nc & 1);          // padded line length of the blocks with nc rows
     const int cF = (n - cls) & 1, cG = cF ^ 1;
-    const int nG = class_size(n, cG);      // the real class cF always has NC members
+    const int nG = class_size(n, cG);      // the real class cF always has nc members
     const int g0 = cG ? 0 : 1;             // class index 0 of E is l = 0: no imaginary part
-    const int kendF = mmax >= cF ? min(NC, ((mmax - cF) >> 1) + 1) : 0;
+    const int kendF = mmax >= cF ? min(nc, ((mmax - cF) >> 1) + 1) : 0;
     const int kendG = mmax >= cG ? min(nG, ((mmax - cG) >> 1) + 1) : 0;
     Real* sm = reinterpret_cast<Real*>(smem_raw);
     const Real* tab = sm + c.tab_off;
@@ -150,101 +199,63 @@ __device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax
     Real* re_io = row + (2 * cF) * L;      // class index k at + 4k L
     Real* im_io = row + (2 * cG - 1) * L;  // class index k at + 4k L (k >= g0)
 
-    Real ure[NC][TL], uim[NC][TL];
+    Real ure[NCE][TL], uim[NCE][TL];
 #pragma unroll
-    for (int i = 0; i < NC; ++i)
+    for (int i = 0; i < NCE; ++i)
 #pragma unroll
         for (int t = 0; t < TL; ++t) ure[i][t] = uim[i][t] = Real(0);
 
-    // ---- first products: u_re = A_F[cls, cF] re[cF],  u_im = A_G[cls, cG] im[cG]
-    const int kend = max(kendF, kendG);
-#pragma unroll 1
-    for (int k = 0; k < kend; ++k) {
-        if (k < kendF) {
-            Real x[TL];
+    // ---- first products: u_re = A_F[cls, cF] re[cF],  u_im = A_G[cls, cG] im[cG].
+    // Software pipelined: the line and the input of step k+1 are in flight while
+    // step k multiplies (a warp can issue a DFMA only every 4 cycles, so with 3
+    // warps per scheduler any exposed shared-memory latency is lost FP64 time).
+    first_product<TL, NCE>(tF1, ld, re_io, 0, kendF, c.local_side && cF == 0, ure);
+    first_product<TL, NCE>(tG1, ld, im_io, g0, kendG, false, uim);
+    // accumulators beyond the class (only when nc < NCE - 1, i.e. NCE == 4 serving
+    // nc <= 2) picked up entries of the following lines: clear them
+    if constexpr (NCE == 4) {
+        if (nc < NCE - 1) {
 #pragma unroll
-            for (int t = 0; t < TL; ++t) x[t] = re_io[4 * k * L + 32 * t];
-            if (c.local_side && k == 0 && cF == 0) {
+            for (int i = 0; i < NCE; ++i)
+                if (i >= nc) {
 #pragma unroll
-                for (int t = 0; t < TL; ++t) x[t] *= Real(0.5);
-            }
-            const Real* line = tF1 + k * LD;
-#pragma unroll
-            for (int i2 = 0; i2 < LD / 2; ++i2) {
-                const Vec2 a = *reinterpret_cast<const Vec2*>(line + 2 * i2);
-#pragma unroll
-                for (int t = 0; t < TL; ++t) ure[2 * i2][t] = fma_(a.x, x[t], ure[2 * i2][t]);
-                if (2 * i2 + 1 < NC) {
-#pragma unroll
-                    for (int t = 0; t < TL; ++t)
-                        ure[2 * i2 + 1][t] = fma_(a.y, x[t], ure[2 * i2 + 1][t]);
+                    for (int t = 0; t < TL; ++t) ure[i][t] = uim[i][t] = Real(0);
                 }
-            }
         }
-        if (k >= g0 && k < kendG) {
-            Real x[TL];
-#pragma unroll
-            for (int t = 0; t < TL; ++t) x[t] = im_io[4 * k * L + 32 * t];
-            const Real* line = tG1 + k * LD;
-#pragma unroll
-            for (int i2 = 0; i2 < LD / 2; ++i2) {
-                const Vec2 a = *reinterpret_cast<const Vec2*>(line + 2 * i2);
-#pragma unroll
-                for (int t = 0; t < TL; ++t) uim[2 * i2][t] = fma_(a.x, x[t], uim[2 * i2][t]);
-                if (2 * i2 + 1 < NC) {
-#pragma unroll
-                    for (int t = 0; t < TL; ++t)
-                        uim[2 * i2 + 1][t] = fma_(a.y, x[t], uim[2 * i2 + 1][t]);
-                }
-            }
-        }
-    }
-    // M2L backward gather signs (-1)^(n+l) (pipeline.cpp:235-239) are constant over a
-    // parity class: applied to the products instead of the inputs (exact)
-    if (c.with_signs) {
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                if (cls) ure[i][t] = -ure[i][t];
-                else uim[i][t] = -uim[i][t];
-            }
     }
     // ---- rotate by +-beta (kernels.cpp:211-217); factors from the global scratch
+    // (the backward pass points c.sb at the negated sines). The M2L backward gather
+    // signs (-1)^(n+l) of pipeline.cpp:235-239 were applied when the z-step stored
+    // its outputs (zstep_task).
     {
         const Real* cbp = c.cb + cls * L;
         const Real* sbp = c.sb + cls * L;
-        Real cm[NC][TL], sn[NC][TL];
 #pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                cm[i][t] = __ldcg(cbp + 2 * i * L + 32 * t);
-                sn[i][t] = __ldcg(sbp + 2 * i * L + 32 * t);
-            }
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
+        for (int i = 0; i < NCE; ++i)
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
-                const Real s = c.negate_sb ? -sn[i][t] : sn[i][t];
+                const Real cm = __ldcg(cbp + 2 * i * L + 32 * t);
+                const Real s = __ldcg(sbp + 2 * i * L + 32 * t);
                 const Real a = ure[i][t], b = uim[i][t];
-                ure[i][t] = fma_(a, cm[i][t], -(b * s));
-                uim[i][t] = fma_(a, s, b * cm[i][t]);
+                ure[i][t] = fma_(a, cm, -(b * s));
+                uim[i][t] = fma_(a, s, b * cm);
             }
     }
     // ---- second products: re[cF] = A_F[cF, cls] u_re,  im[cG] = A_G[cG, cls] u_im.
-    // Output class index r (m' = class + 2r), rows r .. r+3 per trip.
+    // Output class index r (m' = class + 2r), rows r .. r+3 per trip; contracted index
+    // k < nc (u[k] == 0 beyond).
 #pragma unroll 1
-    for (int r = 0; r < NC; r += 4) {
+    for (int r = 0; r < nc; r += 4) {
         Real acc[4][TL];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int t = 0; t < TL; ++t) acc[j][t] = Real(0);
+        const Real* base = tF2 + r;
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-            const Vec2 a0 = *reinterpret_cast<const Vec2*>(tF2 + k * LD + r);
-            const Vec2 a1 = *reinterpret_cast<const Vec2*>(tF2 + k * LD + r + 2);
+        for (int k = 0; k < NCE; ++k) {
+            const Vec2 a0 = *reinterpret_cast<const Vec2*>(base + k * ld);
+            const Vec2 a1 = *reinterpret_cast<const Vec2*>(base + k * ld + 2);
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
                 acc[0][t] = fma_(a0.x, ure[k][t], acc[0][t]);
@@ -259,7 +270,7 @@ __device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (r + j < NC) {
+            if (r + j < nc) {
 #pragma unroll
                 for (int t = 0; t < TL; ++t) re_io[4 * (r + j) * L + 32 * t] = acc[j][t];
             }
@@ -273,7 +284,7 @@ __device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax
             for (int t = 0; t < TL; ++t) acc[j][t] = Real(0);
         const Real* base = tG2 + r;
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
+        for (int k = 0; k < NCE; ++k) {
             const Vec2 a0 = *reinterpret_cast<const Vec2*>(base + k * ldG2);
             const Vec2 a1 = *reinterpret_cast<const Vec2*>(base + k * ldG2 + 2);
 #pragma unroll
@@ -296,23 +307,23 @@ __device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax
 template <int TL>
 __device__ __forceinline__ void half_task_dispatch(const Ctx<TL> c, int n, int cls, int mmax) {
     const int nc = class_size(n, cls);
-    switch (nc) {
-#define SFMM_CASE(K)                                             \
-    case K:                                                      \
-        if constexpr (K <= NCMAX) half_task<TL, K>(c, n, cls, mmax); \
-        break;
-        SFMM_CASE(1) SFMM_CASE(2) SFMM_CASE(3) SFMM_CASE(4) SFMM_CASE(5)
-        SFMM_CASE(6) SFMM_CASE(7) SFMM_CASE(8) SFMM_CASE(9) SFMM_CASE(10)
-#undef SFMM_CASE
-        default: break;
+    if (nc <= 4) half_task<TL, 4>(c, n, cls, mmax);
+    else if (nc <= 6) half_task<TL, 6>(c, n, cls, mmax);
+    else if (nc <= 8) {
+        if constexpr (NCMAX > 6) half_task<TL, 8>(c, n, cls, mmax);
+    } else {
+        if constexpr (NCMAX > 8) half_task<TL, 10>(c, n, cls, mmax);
     }
 }
 
 // z-axis step on column (m, part) in place, R outputs per translation
-// (reference kernels.cpp:118-196). The operator is Hankel (M2L: (2m+i+k)!) or
-// Toeplitz (M2M/L2L), so four k-steps share one sliding window of R+3 entries.
-template <int TL, int R, int DIR>
-__device__ __noinline__ void zstep_task(int buf_off, int zi, int p_in, int p_out, int m, int part) {
+// (reference kernels.cpp:118-196). The Hankel (M2L: (2m+i+k)!) or Toeplitz
+// (M2M/L2L) operator entries come from the constant bank: every warp walks the
+// same ~40-entry table, the access pattern for which the constant path runs at
+// full rate. Kept as a plain k loop for code size (see half_task).
+template <int TL, int R>
+__device__ __noinline__ void zstep_task(int buf_off, int zi, int zstep, int p_in, int p_out, int m,
+                                        int part, bool alternate_signs) {
     constexpr int L = 32 * TL;
     const int kin = p_in - m, kout = p_out - m;
     Real* buf = reinterpret_cast<Real*>(smem_raw) + buf_off + (threadIdx.x & 31);
@@ -322,27 +333,8 @@ __device__ __noinline__ void zstep_task(int buf_off, int zi, int p_in, int p_out
     for (int i = 0; i < R; ++i)
 #pragma unroll
         for (int t = 0; t < TL; ++t) acc[i][t] = Real(0);
-    int k = 0;
-    for (; k + 4 <= kin; k += 4) {
-        Real w[R + 3];
-        const int w0 = DIR > 0 ? zi : zi - 3;
-#pragma unroll
-        for (int j = 0; j < R + 3; ++j) w[j] = c_z[w0 + j];
-        Real x[4][TL];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int t = 0; t < TL; ++t) x[u][t] = col[((2 * m + k + u) * (k + u)) * L + 32 * t];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int i = 0; i < R; ++i)
-#pragma unroll
-                for (int t = 0; t < TL; ++t)
-                    acc[i][t] = fma_(w[(DIR > 0 ? u : 3 - u) + i], x[u][t], acc[i][t]);
-        zi += 4 * DIR;
-    }
-    for (; k < kin; ++k) {
+#pragma unroll 1
+    for (int k = 0; k < kin; ++k) {
         Real x[TL];
 #pragma unroll
         for (int t = 0; t < TL; ++t) x[t] = col[((2 * m + k) * k) * L + 32 * t];
@@ -352,7 +344,15 @@ __device__ __noinline__ void zstep_task(int buf_off, int zi, int p_in, int p_out
 #pragma unroll
             for (int t = 0; t < TL; ++t) acc[i][t] = fma_(a, x[t], acc[i][t]);
         }
-        zi += DIR;
+        zi += zstep;
+    }
+    // M2L: the backward gather multiplies row n, column m by (-1)^(n+m) = (-1)^i
+    // (pipeline.cpp:235-239); negation is exact, so it is applied here once
+    if (alternate_signs) {
+#pragma unroll
+        for (int i = 1; i < R; i += 2)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) acc[i][t] = -acc[i][t];
     }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -368,13 +368,12 @@ __device__ __forceinline__ void zstep_dispatch(int buf, int kind, int p_in, int 
                                                int part) {
     const int r4 = (p_out - m + 3) >> 2;
     const int zi = kind == KIND_M2L ? Z_FAC + 2 * m : (kind == KIND_M2M ? Z_LOW + PMAX : Z_UP + PMAX);
+    const int zstep = kind == KIND_M2L ? 1 : -1;
     switch (r4) {
 #define SFMM_CASE(K)                                                                  \
     case K:                                                                           \
-        if constexpr (4 * K <= PMAX + 3) {                                            \
-            if (kind == KIND_M2L) zstep_task<TL, 4 * K, 1>(buf, zi, p_in, p_out, m, part);  \
-            else zstep_task<TL, 4 * K, -1>(buf, zi, p_in, p_out, m, part);            \
-        }                                                                             \
+        if constexpr (4 * K <= PMAX + 3)                                                \
+            zstep_task<TL, 4 * K>(buf, zi, zstep, p_in, p_out, m, part, kind == KIND_M2L); \
         break;
         SFMM_CASE(1) SFMM_CASE(2) SFMM_CASE(3) SFMM_CASE(4) SFMM_CASE(5)
 #undef SFMM_CASE
@@ -415,11 +414,11 @@ struct TriWalk {
 struct TiledTables {
     const Real* stream[2];  // global parity-block streams: [0] multipole side, [1] local side
     uint32_t bytes[2];      // bytes staged for the forward / backward pass
-    Real* beta;             // global scratch: per CTA cb[p_rot][L], sb[p_rot][L]
+    Real* beta;             // global scratch: per CTA three tables [p_rot + 2][L]
 };
 
 template <int TL>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, int p_rot,
                        int tab_len) {
     constexpr int L = 32 * TL;
@@ -438,8 +437,11 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     uint64_t* mbar =
         reinterpret_cast<uint64_t*>(sm + lay.tab_len + lay.buf_elems() + lay.geo_elems());
     int* counters = reinterpret_cast<int*>(mbar + 1);
-    Real* cbg = tt.beta + (size_t)blockIdx.x * 2 * p_rot * L + lane;
-    Real* sbg = cbg + (size_t)p_rot * L;
+    // per CTA: cos(m beta), sin(m beta), -sin(m beta), each [p_rot + 2][L] (two slack rows:
+    // the NCE code reads one class index past an odd-sized class)
+    Real* cbg = tt.beta + (size_t)blockIdx.x * 3 * (p_rot + 2) * L + lane;
+    Real* sbg = cbg + (size_t)(p_rot + 2) * L;
+    Real* nsbg = sbg + (size_t)(p_rot + 2) * L;
 
     const int kind = a.kind, p_in = a.p_in, p_out = a.p_out;
     const bool src_local = kind == KIND_L2L;
@@ -497,9 +499,10 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
                 geo[2 * L + 32 * t] = ang.rn;
                 geo[3 * L + 32 * t] = Real(1) / ang.rn;
                 Real c = 1, s = 0;
-                for (int m = 0; m < p_rot; ++m) {
+                for (int m = 0; m < p_rot + 2; ++m) {
                     cbg[m * L + 32 * t] = c;
                     sbg[m * L + 32 * t] = s;
+                    nsbg[m * L + 32 * t] = -s;
                     const Real nc = fma_(c, ang.cb, -(s * ang.sb));
                     const Real ns = fma_(s, ang.cb, c * ang.sb);
                     c = nc;
@@ -603,7 +606,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
 
         // ---- B: forward swap passes, largest rows first
         {
-            Ctx<TL> c{(int)lay.tab_len, 0, cbg, sbg, src_local, false, false};
+            Ctx<TL> c{(int)lay.tab_len, 0, cbg, sbg, src_local};
             for (int task = fetch_task(&counters[0], lane); task < 2 * p_in;
                  task = fetch_task(&counters[0], lane)) {
                 const int n = p_in - 1 - (task >> 1);
@@ -635,7 +638,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         // ---- C: backward swap passes; columns >= cols of the z-step output are
         // zero (pipeline.cpp:229-246) and are skipped, which is exact
         {
-            Ctx<TL> c{(int)lay.tab_len, 0, cbg, sbg, dst_local, true, kind == KIND_M2L};
+            Ctx<TL> c{(int)lay.tab_len, 0, cbg, nsbg, dst_local};
             for (int task = fetch_task(&counters[2], lane); task < 2 * p_out;
                  task = fetch_task(&counters[2], lane)) {
                 const int n = p_out - 1 - (task >> 1);
@@ -784,9 +787,9 @@ cudaError_t ensure_constants() {
 int tiled_warps_for(int p_rot) {
     if (const char* env = getenv("SFMM_TILED_WARPS")) {
         const int w = atoi(env);
-        if (w >= 2 && w <= 8) return w;
+        if (w >= 2 && w <= 12) return w;
     }
-    if (p_rot >= 12) return 8;
+    if (p_rot >= 12) return 12;
     return 4;
 }
 
@@ -828,7 +831,7 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     tt.stream[1] = t.stream[1];
     tt.bytes[0] = (uint32_t)(staged(a.p_in) * sizeof(Real));
     tt.bytes[1] = (uint32_t)(staged(a.p_out) * sizeof(Real));
-    e = cudaMallocAsync((void**)&tt.beta, sizeof(Real) * (size_t)grid * 2 * p_rot * L, stream);
+    e = cudaMallocAsync((void**)&tt.beta, sizeof(Real) * (size_t)grid * 3 * (p_rot + 2) * L, stream);
     if (e != cudaSuccess) return e;
     kern<<<grid, block, smem, stream>>>(a, tt, n_groups, p_rot, (int)tab_len);
     e = cudaGetLastError();
