@@ -31,7 +31,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2202_02847_b200 import workloads  # noqa: E402
+from paper_2202_02847_b200 import sharding, workloads  # noqa: E402
 
 P = 20
 GRID = (32, 16, 16)
@@ -100,10 +100,6 @@ class ClockSampler:
                     pass
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
                 "reasons": sorted(reasons), "samples": len(sm)}
-
-
-def shard(n_targets: int, rank: int, world: int):
-    return n_targets * rank // world, n_targets * (rank + 1) // world
 
 
 def build_level(seed: int = 0):
@@ -212,12 +208,9 @@ def main():
 
     sources, tgt_ptr, src_index, shifts = build_level()
     n_targets = len(tgt_ptr) - 1
-    t_lo, t_hi = shard(n_targets, rank, world)
-    pair_lo, pair_hi = int(tgt_ptr[t_lo]), int(tgt_ptr[t_hi])
-    my_ptr = tgt_ptr[t_lo:t_hi + 1] - tgt_ptr[t_lo]
-    my_idx = np.ascontiguousarray(src_index[pair_lo:pair_hi])
-    my_shifts = np.ascontiguousarray(shifts[pair_lo:pair_hi])
-    my_pairs = pair_hi - pair_lo
+    t_lo, t_hi, my_ptr, my_idx, my_shifts = sharding.shard_plan(tgt_ptr, src_index, shifts, rank,
+                                                               world)
+    my_pairs = len(my_idx)
     total_pairs = int(tgt_ptr[-1])
     n_src = len(sources)
     my_targets = t_hi - t_lo

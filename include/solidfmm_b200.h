@@ -67,6 +67,13 @@ const char* sfmm_last_error(void); /* thread-local detail for the last failure *
 sfmm_status sfmm_get_swap_tables(const sfmm_handle* h, int n, double* f, double* g);
 sfmm_status sfmm_get_faculties(const sfmm_handle* h, double* fac, double* inv);
 
+/* The same tables computed on the host without touching a device (what
+ * sfmm_create uploads): wigner_b / swap_matrices (operators.cpp:12-66) and the
+ * faculty tables of operator_data (operators.cpp:134-142). INVALID_ARGUMENT for
+ * n < 0 or an order outside [1, sfmm_max_order(precision)]. */
+sfmm_status sfmm_host_swap_tables(int n, double* f, double* g);
+sfmm_status sfmm_host_faculties(sfmm_precision precision, int order, double* fac, double* inv);
+
 /* ---- batched translation, host buffers, reference AoS layout -------------
  * Replaces m2l/m2m/l2l(ops, span<translation_request>, ws) (pipeline.hpp:30-45,
  * pipeline.cpp:275-369) for one uniform (p_in, p_out) group: validates every

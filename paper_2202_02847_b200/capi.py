@@ -32,6 +32,8 @@ _SIGNATURES = {
     "sfmm_last_error": (c_char_p, []),
     "sfmm_get_swap_tables": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "sfmm_get_faculties": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "sfmm_host_swap_tables": (c_int, [c_int, c_void_p, c_void_p]),
+    "sfmm_host_faculties": (c_int, [c_int, c_int, c_void_p, c_void_p]),
     "sfmm_translate_host": (c_int, [c_void_p, c_int, c_int64, c_int, c_int, c_void_p, c_void_p,
                                     c_void_p]),
     "sfmm_translate_host_mixed": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p,
@@ -110,6 +112,21 @@ def check(status: int) -> None:
 
 def max_order(precision: int) -> int:
     return load_library().sfmm_max_order(precision)
+
+
+def host_swap_tables(n: int):
+    """F_n, G_n as the library builds them, no device needed."""
+    f = np.empty((n + 1, n + 1), np.float64)
+    g = np.empty((n + 1, n + 1), np.float64)
+    check(load_library().sfmm_host_swap_tables(n, _ptr(f), _ptr(g)))
+    return f, g
+
+
+def host_faculties(precision: int, order: int):
+    fac = np.empty(max(2 * order - 1, 1), np.float64)
+    inv = np.empty(max(order, 1), np.float64)
+    check(load_library().sfmm_host_faculties(precision, order, _ptr(fac), _ptr(inv)))
+    return fac, inv
 
 
 def dtype_of(precision: int):

@@ -523,6 +523,33 @@ sfmm_status sfmm_get_faculties(const sfmm_handle* h, double* fac, double* inv) {
     return SFMM_OK;
 }
 
+sfmm_status sfmm_host_swap_tables(int n, double* f, double* g) {
+    if (n < 0 || n >= max_order_f64()) return fail(SFMM_INVALID_ARGUMENT, "row out of range");
+    const SwapTables t(n + 1);
+    if (f) std::copy(t.f[n].begin(), t.f[n].end(), f);
+    if (g) std::copy(t.g[n].begin(), t.g[n].end(), g);
+    return SFMM_OK;
+}
+
+sfmm_status sfmm_host_faculties(sfmm_precision precision, int order, double* fac, double* inv) {
+    if (precision != SFMM_F64 && precision != SFMM_F32)
+        return fail(SFMM_INVALID_ARGUMENT, "unknown precision");
+    if (order < 1 || order > sfmm_max_order(precision))
+        return fail(SFMM_INVALID_ARGUMENT, "order out of range");
+    if (precision == SFMM_F64) {
+        std::vector<double> a, b;
+        build_faculties<double>(order, a, b);
+        if (fac) std::copy(a.begin(), a.end(), fac);
+        if (inv) std::copy(b.begin(), b.end(), inv);
+    } else {
+        std::vector<float> a, b;
+        build_faculties<float>(order, a, b);
+        if (fac) std::copy(a.begin(), a.end(), fac);
+        if (inv) std::copy(b.begin(), b.end(), inv);
+    }
+    return SFMM_OK;
+}
+
 sfmm_status sfmm_translate_host(sfmm_handle* h, sfmm_kind kind, int64_t n, int p_in, int p_out,
                                 const void* in_aos, const void* shifts, void* out_aos) {
     if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");

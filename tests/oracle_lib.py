@@ -134,8 +134,8 @@ class Oracle(_Base):
         return f, g
 
     def faculties(self, order, dtype=np.float64):
-        fac = np.zeros(2 * order - 1, dtype)
-        inv = np.zeros(order, dtype)
+        fac = np.zeros(max(2 * order - 1, 1), dtype)
+        inv = np.zeros(max(order, 1), dtype)
         fn = self.lib.orc_faculties_f64 if dtype == np.float64 else self.lib.orc_faculties_f32
         st = fn(c_int(order), _p(fac), _p(inv))
         return st, fac, inv
@@ -238,8 +238,8 @@ class Reference(_Base):
         return b, f, g
 
     def faculties(self, order, dtype=np.float64):
-        fac = np.zeros(2 * order - 1, dtype)
-        inv = np.zeros(order, dtype)
+        fac = np.zeros(max(2 * order - 1, 1), dtype)
+        inv = np.zeros(max(order, 1), dtype)
         fn = self.lib.ref_faculties_f64 if dtype == np.float64 else self.lib.ref_faculties_f32
         st = fn(c_int(order), _p(fac), _p(inv))
         return st, fac, inv

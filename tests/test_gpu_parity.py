@@ -1,0 +1,298 @@
+"""Parity of the CUDA library against the CPU oracle, through the C ABI, on a
+B200. Bit-exact (numeric equality of every coefficient) wherever the reference
+defines the result; tolerances are written out where a different quantity is
+compared (accuracy against the O(P^4) kernel, summation order)."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2202_02847_b200 import capi, sharding, workloads
+from tests.helpers import bits_equal, random_shifts, random_solids, solid_size
+from tests.oracle_lib import normalized_error
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).parent / "golden"
+KINDS = {"m2l": capi.M2L, "m2m": capi.M2M, "l2l": capi.L2L}
+GENERIC, TILED = 1, 2
+
+
+@pytest.fixture(scope="module")
+def h64():
+    h = capi.Handle(capi.F64, 30)
+    yield h
+    h.close()
+
+
+@pytest.fixture(scope="module")
+def h32():
+    h = capi.Handle(capi.F32, 18)
+    yield h
+    h.close()
+
+
+def run(h, kind, p_in, p_out, src, sh, variant=0):
+    h.set_option("kernel_variant", variant)
+    try:
+        return h.translate_host(KINDS[kind], p_in, p_out, src, sh)
+    finally:
+        h.set_option("kernel_variant", 0)
+
+
+# ---- random requests, every kind, both kernels -----------------------------
+
+@pytest.mark.parametrize("variant", [GENERIC, TILED], ids=["generic", "tiled"])
+def test_random_mixed_orders_f64(oracle, h64, variant):
+    rng = np.random.default_rng(7)
+    pmax = 30 if variant == GENERIC else 20
+    for trial in range(30):
+        kind = ("m2l", "m2m", "l2l")[trial % 3]
+        p_in, p_out = int(rng.integers(1, pmax + 1)), int(rng.integers(1, pmax + 1))
+        if trial < 4:
+            p_in = p_out = (1, 2, pmax, pmax)[trial]
+        n = int(rng.integers(1, 200))
+        x, sh = random_solids(rng, n, p_in), random_shifts(rng, n)
+        st, want = oracle.translate(kind, p_in, p_out, x, sh)
+        assert st == 0
+        assert bits_equal(run(h64, kind, p_in, p_out, x, sh, variant), want), (kind, p_in, p_out, n)
+
+
+@pytest.mark.parametrize("variant", [GENERIC, TILED], ids=["generic", "tiled"])
+def test_random_mixed_orders_f32(oracle, h32, variant):
+    rng = np.random.default_rng(8)
+    for trial in range(24):
+        kind = ("m2l", "m2m", "l2l")[trial % 3]
+        p_in, p_out = int(rng.integers(1, 19)), int(rng.integers(1, 19))
+        n = int(rng.integers(1, 200))
+        x, sh = random_solids(rng, n, p_in, np.float32, 0.05), random_shifts(rng, n, dtype=np.float32)
+        st, want = oracle.translate(kind, p_in, p_out, x, sh, np.float32)
+        assert st == 0
+        assert bits_equal(run(h32, kind, p_in, p_out, x, sh, variant), want), (kind, p_in, p_out, n)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 63, 64, 65, 129])
+def test_group_boundaries(oracle, h64, n):
+    rng = np.random.default_rng(n)
+    x, sh = random_solids(rng, n, 11), random_shifts(rng, n)
+    _, want = oracle.translate("m2l", 11, 9, x, sh)
+    for variant in (GENERIC, TILED):
+        assert bits_equal(run(h64, "m2l", 11, 9, x, sh, variant), want)
+
+
+# ---- BASELINE.json configs at sizes the oracle finishes in seconds ----------
+
+def test_config0_m2l_f64_p8(oracle, h64):
+    src, sh = workloads.config0(0, 4096, 8)
+    got = run(h64, "m2l", 8, 8, src, sh)
+    _, want = oracle.translate("m2l", 8, 8, src, sh)
+    assert bits_equal(got, want)
+    _, naive = oracle.m2l_naive(8, 8, src[:512], sh[:512])
+    assert normalized_error(got[:512], naive) < 1e-12      # accuracy oracle
+
+
+def test_config1_m2m_l2l_f64_p16(oracle, h64):
+    src, sh = workloads.config1(0, 2048, 16)
+    got = run(h64, "m2m", 16, 16, src, sh)
+    assert bits_equal(got, oracle.translate("m2m", 16, 16, src, sh)[1])
+    msrc, msh = workloads.config0(1, 2048, 16)
+    loc = run(h64, "m2l", 16, 16, msrc, msh)
+    assert bits_equal(loc, oracle.translate("m2l", 16, 16, msrc, msh)[1])
+    got = run(h64, "l2l", 16, 16, loc, sh)
+    assert bits_equal(got, oracle.translate("l2l", 16, 16, loc, sh)[1])
+
+
+def test_config2_m2l_f32_p6(oracle, h32):
+    src, sh = workloads.config2(0, 8192, 6)
+    got = run(h32, "m2l", 6, 6, src, sh)
+    assert bits_equal(got, oracle.translate("m2l", 6, 6, src, sh, np.float32)[1])
+    _, naive = oracle.m2l_naive(6, 6, src[:512].astype(np.float64), sh[:512].astype(np.float64))
+    assert normalized_error(got[:512], naive) < 1e-5       # north_star FP32 tolerance
+
+
+@pytest.mark.parametrize("variant", [GENERIC, TILED], ids=["generic", "tiled"])
+def test_config3_level_accumulation(oracle, h64, variant):
+    p = 20
+    src, tgt_ptr, idx, sh = workloads.config3(0, (2, 2, 3), p)
+    h64.set_option("kernel_variant", variant)
+    try:
+        plan = h64.plan(tgt_ptr, idx, sh, len(src))
+        assert plan.pairs == len(idx)
+        got = plan.accumulate_host(p, p, src)
+        plan.close()
+    finally:
+        h64.set_option("kernel_variant", 0)
+    _, per_pair = oracle.translate("m2l", p, p, src[idx], sh)
+    if variant == TILED:
+        # groups of 64 pairs, documented tree (sharding.accumulation_tree): bit exact
+        assert bits_equal(got, sharding.accumulation_tree(per_pair, tgt_ptr))
+    # any summation order of the same terms: 189 terms, a few ulp of the largest
+    seq = np.add.reduceat(per_pair, tgt_ptr[:-1], axis=0)
+    assert normalized_error(got, seq) < 1e-13
+
+
+def test_config4_mixed_orders_and_sweep(oracle, h64):
+    for p_in, p_out, seed in ((24, 12, 2), (12, 24, 3)):
+        src, sh = workloads.config0(seed, 256, p_in)
+        assert bits_equal(run(h64, "m2l", p_in, p_out, src, sh), oracle.translate("m2l", p_in, p_out, src, sh)[1])
+    for p in range(2, 31):
+        src, sh = workloads.config0(100 + p, 96, p)
+        assert bits_equal(run(h64, "m2l", p, p, src, sh), oracle.translate("m2l", p, p, src, sh)[1]), p
+
+
+def test_mixed_order_batch_call(oracle, h64):
+    rng = np.random.default_rng(53)
+    n = 300
+    p_in = rng.integers(1, 25, n).astype(np.int32)
+    p_out = rng.integers(1, 25, n).astype(np.int32)
+    in_off = np.concatenate([[0], np.cumsum([solid_size(p) for p in p_in])]).astype(np.int64)
+    out_off = np.concatenate([[0], np.cumsum([solid_size(p) for p in p_out])]).astype(np.int64)
+    src = np.concatenate([random_solids(rng, 1, int(p))[0] for p in p_in])
+    sh = random_shifts(rng, n)
+    for kind in ("m2l", "m2m", "l2l"):
+        st, want = oracle.translate_mixed(kind, p_in, p_out, src, in_off[:-1], sh, int(out_off[-1]), out_off[:-1])
+        out = np.full(int(out_off[-1]), np.nan)
+        h64.translate_host_mixed(KINDS[kind], p_in, p_out, src, in_off[:-1], sh, out, out_off[:-1])
+        assert bits_equal(out, want)
+
+
+# ---- golden fixtures generated from the unmodified reference ----------------
+
+@pytest.mark.parametrize("path", sorted(GOLDEN.glob("*.npz")), ids=lambda p: p.stem)
+def test_golden_fixture(h64, h32, path):
+    z = np.load(path)
+    h = h32 if z["src"].dtype == np.float32 else h64
+    if "p_in_each" in z.files:
+        out = np.empty(len(z["out"]), z["src"].dtype)
+        h.translate_host_mixed(KINDS[str(z["kind"])], z["p_in_each"], z["p_out_each"], z["src"], z["in_off"],
+                               z["shifts"], out, z["out_off"])
+        assert bits_equal(out, z["out"])
+        return
+    p_in, p_out = int(z["p_in"]), int(z["p_out"])
+    for variant in (GENERIC, TILED):
+        if variant == TILED and max(p_in, p_out) > (18 if h is h32 else 20):
+            continue
+        assert bits_equal(run(h, str(z["kind"]), p_in, p_out, z["src"], z["shifts"], variant), z["out"])
+
+
+# ---- full-size runs: size-independent properties ---------------------------
+
+def test_full_config0_permutation_and_linearity(oracle, h64):
+    n = 65536
+    src, sh = workloads.config0(0, n, 8)
+    out = run(h64, "m2l", 8, 8, src, sh)
+    perm = np.random.default_rng(0).permutation(n)
+    assert bits_equal(run(h64, "m2l", 8, 8, src[perm], sh[perm]), out[perm])   # position independent
+    sel = np.arange(0, n, 997)
+    assert bits_equal(out[sel], oracle.translate("m2l", 8, 8, src[sel], sh[sel])[1])
+    lin = run(h64, "m2l", 8, 8, 1.7 * src[:4096] - 0.6 * src[4096:8192], sh[:4096])
+    ref_lin = 1.7 * out[:4096] - 0.6 * run(h64, "m2l", 8, 8, src[4096:8192], sh[:4096])
+    assert normalized_error(lin, ref_lin) < 1e-13                               # test_pipeline.cpp:116-134
+
+
+def test_full_config1_round_trips(oracle, h64):
+    n = 2 ** 18
+    src, sh = workloads.config1(0, n, 16)
+    there = run(h64, "m2m", 16, 16, src, sh)
+    back = run(h64, "m2m", 16, 16, there, -sh)
+    assert normalized_error(back, src) < 1e-12                                  # test_pipeline.cpp:185-188
+    sel = np.arange(0, n, 4099)
+    assert bits_equal(there[sel], oracle.translate("m2m", 16, 16, src[sel], sh[sel])[1])
+    loc = run(h64, "m2l", 16, 16, src[:32768], workloads.config0(5, 32768, 1)[1])
+    moved = run(h64, "l2l", 16, 16, loc, sh[:32768])
+    assert normalized_error(run(h64, "l2l", 16, 16, moved, -sh[:32768]), loc) < 2e-11  # L2L floor, SURVEY §7.1
+
+
+def test_full_config3_level(oracle, h64):
+    p = 20
+    src, tgt_ptr, idx, sh = workloads.config3(0, (32, 16, 16), p)
+    plan = h64.plan(tgt_ptr, idx, sh, len(src))
+    out = plan.accumulate_host(p, p, src)
+    plan.close()
+    assert out.shape == (8192, solid_size(p)) and np.all(np.isfinite(out))
+    for t in (0, 777, 4096, 8191):                                              # spot targets, exact
+        sl = slice(int(tgt_ptr[t]), int(tgt_ptr[t + 1]))
+        _, per_pair = oracle.translate("m2l", p, p, src[idx[sl]], sh[sl])
+        want = sharding.accumulation_tree(per_pair, np.array([0, 189]))
+        assert bits_equal(out[t], want[0]), t
+    # a checksum of checksums: the level is linear in the sources
+    out2 = h64.plan(tgt_ptr, idx, sh, len(src)).accumulate_host(p, p, 2.0 * src)
+    assert bits_equal(out2, 2.0 * out)                                          # scaling by 2 is exact
+
+
+# ---- API contracts ---------------------------------------------------------
+
+def test_error_contracts(h64):
+    rng = np.random.default_rng(79)
+    m = random_solids(rng, 3, 6)
+    good = random_shifts(rng, 3, with_axes=False)
+    bad = good.copy()
+    bad[1] = 0.0
+    for kind in KINDS.values():
+        out = np.full((3, solid_size(6)), 7.0)
+        with pytest.raises(capi.DomainError):
+            h64.translate_host(kind, 6, 6, m, bad, out)
+        assert np.all(out == 7.0)                       # nothing written (pipeline.cpp:282-298)
+    with pytest.raises(capi.InvalidArgument):
+        h64.translate_host(capi.M2L, 6, 31, m, good)    # order exceeds operator data order
+    with pytest.raises(capi.InvalidArgument):
+        h64.translate_host(capi.M2L, 0, 6, m, good)
+    small = capi.Handle(capi.F64, 4)
+    with pytest.raises(capi.InvalidArgument):
+        small.translate_host(capi.M2L, 6, 4, m, good)
+    small.close()
+    assert h64.translate_host(capi.M2L, 6, 6, m[:0], good[:0]).shape == (0, solid_size(6))  # empty batch
+    with pytest.raises(capi.DomainError):
+        h64.plan([0, 2], [0, 1], [[1.0, 0, 0], [0.0, 0, 0]], 2)
+    with pytest.raises(capi.InvalidArgument):
+        h64.plan([0, 2], [0, 5], [[1.0, 0, 0], [1.0, 0, 0]], 2)
+
+
+def test_in_place(oracle, h64):
+    rng = np.random.default_rng(73)
+    m = random_solids(rng, 100, 8)
+    sh = random_shifts(rng, 100)
+    want = oracle.translate("m2m", 8, 8, m, sh)[1]
+    buf = m.copy()
+    h64.translate_host(capi.M2M, 8, 8, buf, sh, buf)    # output aliases the source
+    assert bits_equal(buf, want)
+
+
+def test_handle_tables_and_device_soa_path(oracle, h64):
+    import torch
+    f, g = h64.swap_tables(19)
+    fo, go = oracle.swap_tables(19)
+    assert np.array_equal(f, fo) and np.array_equal(g, go)
+    fac, inv = capi.Handle(capi.F64, 3).faculties()
+    assert fac.tolist() == [1.0, 1.0, 2.0, 6.0, 24.0]
+    # device-resident SoA call with the zero-shift scan on the device
+    rng = np.random.default_rng(5)
+    n, p = 500, 12
+    x, sh = random_solids(rng, n, p), random_shifts(rng, n)
+    dev = torch.device("cuda", 0)
+    stride = 512
+    d_aos = torch.from_numpy(x).to(dev)
+    d_in = torch.zeros((solid_size(p), stride), dtype=torch.float64, device=dev)
+    d_out = torch.full((solid_size(p), stride), 3.0, dtype=torch.float64, device=dev)
+    d_sh = torch.from_numpy(sh).to(dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    h64.pack_soa(n, p, d_aos.data_ptr(), d_in.data_ptr(), stride, stream)
+    h64.translate_soa(capi.M2L, n, p, p, d_in.data_ptr(), stride, d_sh.data_ptr(), d_out.data_ptr(), stride, stream)
+    d_back = torch.empty((n, solid_size(p)), dtype=torch.float64, device=dev)
+    h64.unpack_soa(n, p, d_out.data_ptr(), stride, d_back.data_ptr(), stream)
+    torch.cuda.synchronize()
+    assert bits_equal(d_back.cpu().numpy(), oracle.translate("m2l", p, p, x, sh)[1])
+    assert torch.all(d_out[:, n:] == 3.0)               # padding columns untouched
+    # a zero shift: DOMAIN_ERROR from the device scan and no write, sync and async
+    bad = sh.copy()
+    bad[77] = 0.0
+    d_sh.copy_(torch.from_numpy(bad))
+    d_out.fill_(5.0)
+    with pytest.raises(capi.DomainError):
+        h64.translate_soa(capi.M2L, n, p, p, d_in.data_ptr(), stride, d_sh.data_ptr(), d_out.data_ptr(), stride, stream)
+    h64.translate_soa(capi.M2L, n, p, p, d_in.data_ptr(), stride, d_sh.data_ptr(), d_out.data_ptr(), stride, stream,
+                      capi.ASYNC_STATUS)
+    with pytest.raises(capi.DomainError):
+        h64.stream_status(stream)
+    assert torch.all(d_out == 5.0)
+    assert h64.launch_count > 0
