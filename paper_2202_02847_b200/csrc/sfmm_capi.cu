@@ -46,6 +46,7 @@ struct DeviceGuard {
 };
 
 constexpr int kFlagSlots = 256;
+constexpr int kPlanGroup = 64;  // pairs of one target are padded to multiples of this
 
 int64_t round_up32(int64_t n) { return (n + 31) / 32 * 32; }
 int64_t solid_len(int p) { return (int64_t)p * (p + 1); }
@@ -76,8 +77,8 @@ struct sfmm_plan {
     sfmm_handle* h = nullptr;
     int64_t n_targets = 0, n_pairs = 0, n_groups = 0, n_sources = 0;
     int64_t* d_grp_ptr = nullptr;   // [n_targets + 1]
-    int32_t* d_src_index = nullptr; // [n_groups * 32], -1 = idle lane
-    void* d_shifts = nullptr;       // [n_groups * 32][3]
+    int32_t* d_src_index = nullptr; // [n_groups * 64], -1 = idle lane
+    void* d_shifts = nullptr;       // [n_groups * 64][3]
 };
 
 namespace {
@@ -290,18 +291,18 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
     for (int64_t t = 0; t < n_targets; ++t) {
         const int64_t cnt = tgt_ptr[t + 1] - tgt_ptr[t];
         if (cnt < 0) return fail(SFMM_INVALID_ARGUMENT, "tgt_ptr must be non-decreasing");
-        grp_ptr[(size_t)t + 1] = grp_ptr[(size_t)t] + (cnt + 31) / 32;
+        grp_ptr[(size_t)t + 1] = grp_ptr[(size_t)t] + (cnt + kPlanGroup - 1) / kPlanGroup;
     }
     const int64_t n_groups = grp_ptr[(size_t)n_targets];
-    std::vector<int32_t> si((size_t)n_groups * 32, -1);
-    std::vector<Real> sh((size_t)n_groups * 32 * 3);
-    for (size_t i = 0; i < (size_t)n_groups * 32; ++i) {
+    std::vector<int32_t> si((size_t)n_groups * kPlanGroup, -1);
+    std::vector<Real> sh((size_t)n_groups * kPlanGroup * 3);
+    for (size_t i = 0; i < (size_t)n_groups * kPlanGroup; ++i) {
         sh[3 * i] = 0;
         sh[3 * i + 1] = 0;
         sh[3 * i + 2] = 1;
     }
     for (int64_t t = 0; t < n_targets; ++t) {
-        int64_t dst = grp_ptr[(size_t)t] * 32;
+        int64_t dst = grp_ptr[(size_t)t] * kPlanGroup;
         for (int64_t j = tgt_ptr[t]; j < tgt_ptr[t + 1]; ++j, ++dst) {
             if (src_index[j] < 0 || src_index[j] >= n_sources)
                 return fail(SFMM_INVALID_ARGUMENT, "source index out of range");
@@ -332,19 +333,22 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
                             const Real* d_src, int64_t src_stride, Real* d_out,
                             int64_t out_stride, cudaStream_t stream) {
     const int64_t so = solid_len(p_out);
-    Real* partial = nullptr;
-    if (plan->n_groups > 0)
-        CU(cudaMallocAsync((void**)&partial, sizeof(Real) * so * plan->n_groups, stream));
     TranslateArgs<Real> a;
     a.kind = KIND_M2L;
     a.p_in = p_in;
     a.p_out = p_out;
-    a.n = plan->n_groups * 32;
+    a.variant = h->variant;
+    // the kernel reduces the lanes of one of ITS groups (32 or 64 pairs) into one partial
+    const int per = kPlanGroup / translate_group_size<Real>(a);
+    const int64_t n_partial = plan->n_groups * per;
+    Real* partial = nullptr;
+    if (n_partial > 0) CU(cudaMallocAsync((void**)&partial, sizeof(Real) * so * n_partial, stream));
+    a.n = plan->n_groups * kPlanGroup;
     a.in = d_src;
     a.in_stride = src_stride;
     a.shifts = static_cast<const Real*>(plan->d_shifts);
     a.out = partial;
-    a.out_stride = plan->n_groups;
+    a.out_stride = n_partial;
     a.src_index = plan->d_src_index;
     a.variant = h->variant;
     a.phase_clocks = h->d_phase_clocks;
@@ -352,7 +356,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     cudaError_t e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
     h->launches += info.launches;
     if (e == cudaSuccess) {
-        e = launch_reduce_groups<Real>(partial, plan->n_groups, plan->d_grp_ptr, plan->n_targets,
+        e = launch_reduce_groups<Real>(partial, n_partial, plan->d_grp_ptr, per, plan->n_targets,
                                        p_out, d_out, out_stride, stream);
         h->launches += 1;
     }

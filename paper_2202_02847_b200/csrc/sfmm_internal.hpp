@@ -46,8 +46,13 @@ struct LaunchInfo {
     int grid = 0, block = 0;
     size_t smem = 0;
     int launches = 0;
+    int group = 32;  // translations per CTA group (accumulate mode: lanes reduced into one partial)
     const char* variant = "";
 };
+
+// Group size the kernel chosen for `a` works with (32 generic, 64 tiled).
+template <typename Real>
+int translate_group_size(const TranslateArgs<Real>& a);
 
 // Translation kernels. Returns cudaSuccess or the launch error.
 template <typename Real>
@@ -79,10 +84,10 @@ cudaError_t launch_unpack_soa(const Real* soa, Real* aos, int64_t n, int p, int6
                               cudaStream_t stream);
 
 // Accumulate mode, second stage: out[c][t] = sum_{g in groups of t} partial[c][g],
-// groups in ascending order. grp_ptr: [n_targets + 1].
+// groups in ascending order. grp_ptr: [n_targets + 1] in units of `per` partial groups.
 template <typename Real>
 cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const int64_t* grp_ptr,
-                                 int64_t n_targets, int p_out, Real* out, int64_t out_stride,
-                                 cudaStream_t stream);
+                                 int per, int64_t n_targets, int p_out, Real* out,
+                                 int64_t out_stride, cudaStream_t stream);
 
 }  // namespace sfmm

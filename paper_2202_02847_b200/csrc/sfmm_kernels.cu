@@ -53,8 +53,9 @@ __global__ void repack_kernel(const Real* __restrict__ src, Real* __restrict__ d
 
 template <typename Real>
 __global__ void reduce_groups_kernel(const Real* __restrict__ partial, int64_t n_groups,
-                                     const int64_t* __restrict__ grp_ptr, int64_t n_targets,
-                                     int S, Real* __restrict__ out, int64_t out_stride) {
+                                     const int64_t* __restrict__ grp_ptr, int per,
+                                     int64_t n_targets, int S, Real* __restrict__ out,
+                                     int64_t out_stride) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int c = blockIdx.y;
     if (t >= n_targets) return;
@@ -64,7 +65,7 @@ __global__ void reduce_groups_kernel(const Real* __restrict__ partial, int64_t n
     while ((n + 1) * (n + 2) <= c) ++n;
     const bool im0 = (c == n * (n + 1) + 1);
     if (!im0) {
-        const int64_t g0 = grp_ptr[t], g1 = grp_ptr[t + 1];
+        const int64_t g0 = grp_ptr[t] * per, g1 = grp_ptr[t + 1] * per;
         for (int64_t g = g0; g < g1; ++g) acc += partial[(int64_t)c * n_groups + g];
     }
     out[(int64_t)c * out_stride + t] = acc;
@@ -163,14 +164,19 @@ cudaError_t launch_unpack_soa(const Real* soa, Real* aos, int64_t n, int p, int6
 
 template <typename Real>
 cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const int64_t* grp_ptr,
-                                 int64_t n_targets, int p_out, Real* out, int64_t out_stride,
-                                 cudaStream_t stream) {
+                                 int per, int64_t n_targets, int p_out, Real* out,
+                                 int64_t out_stride, cudaStream_t stream) {
     if (n_targets <= 0) return cudaSuccess;
     const int S = p_out * (p_out + 1);
     dim3 grid((unsigned)((n_targets + 127) / 128), (unsigned)S), block(128);
     reduce_groups_kernel<Real>
-        <<<grid, block, 0, stream>>>(partial, n_groups, grp_ptr, n_targets, S, out, out_stride);
+        <<<grid, block, 0, stream>>>(partial, n_groups, grp_ptr, per, n_targets, S, out, out_stride);
     return cudaGetLastError();
+}
+
+template <typename Real>
+int translate_group_size(const TranslateArgs<Real>& a) {
+    return (a.variant != 1 && tiled_supports(a)) ? 64 : kLanes;
 }
 
 template <typename Real>
@@ -227,8 +233,9 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
                                                cudaStream_t);                                   \
     template cudaError_t launch_unpack_soa<Real>(const Real*, Real*, int64_t, int, int64_t,     \
                                                  cudaStream_t);                                 \
-    template cudaError_t launch_reduce_groups<Real>(const Real*, int64_t, const int64_t*,       \
+    template cudaError_t launch_reduce_groups<Real>(const Real*, int64_t, const int64_t*, int,  \
                                                     int64_t, int, Real*, int64_t, cudaStream_t); \
+    template int translate_group_size<Real>(const TranslateArgs<Real>&);                        \
     template cudaError_t launch_translate<Real>(const DeviceTables<Real>&,                      \
                                                 const TranslateArgs<Real>&, int, cudaStream_t,  \
                                                 LaunchInfo*);
