@@ -321,9 +321,9 @@ __device__ __forceinline__ void half_task_dispatch(const Ctx<TL> c, int n, int c
 // (M2M/L2L) operator entries come from the constant bank: every warp walks the
 // same ~40-entry table, the access pattern for which the constant path runs at
 // full rate. Kept as a plain k loop for code size (see half_task).
-template <int TL, int R>
-__device__ __noinline__ void zstep_task(int buf_off, int zi, int zstep, int p_in, int p_out, int m,
-                                        int part, bool alternate_signs) {
+template <int TL, int R, int DIR>
+__device__ __noinline__ void zstep_task(int buf_off, int zi, int p_in, int p_out, int m, int part,
+                                        bool alternate_signs) {
     constexpr int L = 32 * TL;
     const int kin = p_in - m, kout = p_out - m;
     Real* buf = reinterpret_cast<Real*>(smem_raw) + buf_off + (threadIdx.x & 31);
@@ -333,8 +333,30 @@ __device__ __noinline__ void zstep_task(int buf_off, int zi, int zstep, int p_in
     for (int i = 0; i < R; ++i)
 #pragma unroll
         for (int t = 0; t < TL; ++t) acc[i][t] = Real(0);
+    // four k-steps share one sliding window of R + 3 operator entries
+    int k = 0;
 #pragma unroll 1
-    for (int k = 0; k < kin; ++k) {
+    for (; k + 4 <= kin; k += 4) {
+        Real w[R + 3];
+        const int w0 = DIR > 0 ? zi : zi - 3;
+#pragma unroll
+        for (int j = 0; j < R + 3; ++j) w[j] = c_z[w0 + j];
+        Real x[4][TL];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int t = 0; t < TL; ++t) x[u][t] = col[((2 * m + k + u) * (k + u)) * L + 32 * t];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+#pragma unroll
+                for (int t = 0; t < TL; ++t)
+                    acc[i][t] = fma_(w[(DIR > 0 ? u : 3 - u) + i], x[u][t], acc[i][t]);
+        zi += 4 * DIR;
+    }
+#pragma unroll 1
+    for (; k < kin; ++k) {
         Real x[TL];
 #pragma unroll
         for (int t = 0; t < TL; ++t) x[t] = col[((2 * m + k) * k) * L + 32 * t];
@@ -344,7 +366,7 @@ __device__ __noinline__ void zstep_task(int buf_off, int zi, int zstep, int p_in
 #pragma unroll
             for (int t = 0; t < TL; ++t) acc[i][t] = fma_(a, x[t], acc[i][t]);
         }
-        zi += zstep;
+        zi += DIR;
     }
     // M2L: the backward gather multiplies row n, column m by (-1)^(n+m) = (-1)^i
     // (pipeline.cpp:235-239); negation is exact, so it is applied here once
@@ -368,12 +390,13 @@ __device__ __forceinline__ void zstep_dispatch(int buf, int kind, int p_in, int 
                                                int part) {
     const int r4 = (p_out - m + 3) >> 2;
     const int zi = kind == KIND_M2L ? Z_FAC + 2 * m : (kind == KIND_M2M ? Z_LOW + PMAX : Z_UP + PMAX);
-    const int zstep = kind == KIND_M2L ? 1 : -1;
     switch (r4) {
-#define SFMM_CASE(K)                                                                  \
-    case K:                                                                           \
-        if constexpr (4 * K <= PMAX + 3)                                                \
-            zstep_task<TL, 4 * K>(buf, zi, zstep, p_in, p_out, m, part, kind == KIND_M2L); \
+#define SFMM_CASE(K)                                                                       \
+    case K:                                                                                \
+        if constexpr (4 * K <= PMAX + 3) {                                                 \
+            if (kind == KIND_M2L) zstep_task<TL, 4 * K, 1>(buf, zi, p_in, p_out, m, part, true);   \
+            else zstep_task<TL, 4 * K, -1>(buf, zi, p_in, p_out, m, part, false);          \
+        }                                                                                  \
         break;
         SFMM_CASE(1) SFMM_CASE(2) SFMM_CASE(3) SFMM_CASE(4) SFMM_CASE(5)
 #undef SFMM_CASE
@@ -393,9 +416,8 @@ struct TiledLayout {
     int p_rot;
     size_t tab_len;  // staged stream elements (prefix + TAB_PAD, multiple of 4)
     __host__ __device__ size_t buf_elems() const { return (size_t)p_rot * p_rot * L; }
-    __host__ __device__ size_t geo_elems() const { return (size_t)4 * L; }
     __host__ __device__ size_t smem_bytes() const {
-        return sizeof(Real) * (buf_elems() + tab_len + geo_elems()) + 32;
+        return sizeof(Real) * (buf_elems() + tab_len) + 32;
     }
 };
 
@@ -414,8 +436,114 @@ struct TriWalk {
 struct TiledTables {
     const Real* stream[2];  // global parity-block streams: [0] multipole side, [1] local side
     uint32_t bytes[2];      // bytes staged for the forward / backward pass
-    Real* beta;             // global scratch: per CTA three tables [p_rot + 2][L]
+    Real* scratch;          // global, per CTA and group parity: geometry of the group (geo_elems)
 };
+
+// Per-group geometry in the global scratch (L2 resident, written one group ahead,
+// reference pipeline.cpp:52-91). Rows of L = 32*TL values:
+//   cos(m beta), sin(m beta), -sin(m beta)   [p_rot + 2] each (two slack rows: the NCE
+//                                            code reads one class index past an odd class)
+//   cos(m alpha), sin(m alpha)               [p_rot] each
+//   qa[m], qd[m]                             [p_rot] each: scale of element (m, m) in the
+//                                            forward / backward pass (head of column m)
+//   base_a, base_d                           the per-row factor of those scales
+template <int TL>
+__host__ __device__ constexpr size_t geo_elems(int p_rot) {
+    return (size_t)(3 * (p_rot + 2) + 4 * p_rot + 2) * 32 * TL;
+}
+
+template <int TL>
+struct GeoView {
+    const Real *cb, *sb, *nsb, *ca, *sa, *qa, *qd, *base_a, *base_d;
+    __device__ GeoView(const Real* g, int p_rot) {
+        constexpr int L = 32 * TL;
+        cb = g;
+        sb = cb + (size_t)(p_rot + 2) * L;
+        nsb = sb + (size_t)(p_rot + 2) * L;
+        ca = nsb + (size_t)(p_rot + 2) * L;
+        sa = ca + (size_t)p_rot * L;
+        qa = sa + (size_t)p_rot * L;
+        qd = qa + (size_t)p_rot * L;
+        base_a = qd + (size_t)p_rot * L;
+        base_d = base_a + L;
+    }
+};
+
+// Geometry of one group: warp t fills slot set t. Scales (pipeline.cpp:148-154, 251-257):
+// forward |r|^n (local source) or |r|^-(n+1); backward |r|^-n (local target) or |r|^(n+1);
+// all powers by repeated multiplication from 1 (pipeline.cpp:81-89).
+template <int TL>
+__device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int64_t g, int p_rot,
+                                               Real* geo, bool src_local, bool dst_local, int warp,
+                                               int lane) {
+    constexpr int L = 32 * TL;
+    if (warp >= TL) return;
+    const int t = warp;
+    const int64_t b = g * L + 32 * t + lane;
+    bool active = b < a.n;
+    if (active && a.src_index) active = a.src_index[b] >= 0;
+    Real x = 0, y = 0, z = 1;  // idle lanes get a benign shift (pipeline.cpp:56-61)
+    if (active) {
+        x = a.shifts[3 * b];
+        y = a.shifts[3 * b + 1];
+        z = a.shifts[3 * b + 2];
+    }
+    const Angles<Real> ang = decompose_angles(x, y, z);
+    const GeoView<TL> v(geo + 32 * t + lane, p_rot);
+    Real* cbg = const_cast<Real*>(v.cb);
+    Real* sbg = const_cast<Real*>(v.sb);
+    Real* nsbg = const_cast<Real*>(v.nsb);
+    Real* cag = const_cast<Real*>(v.ca);
+    Real* sag = const_cast<Real*>(v.sa);
+    Real* qag = const_cast<Real*>(v.qa);
+    Real* qdg = const_cast<Real*>(v.qd);
+    const Real inv = Real(1) / ang.rn;
+    const Real base_a = src_local ? ang.rn : inv;
+    const Real base_d = dst_local ? inv : ang.rn;
+    *const_cast<Real*>(v.base_a) = base_a;
+    *const_cast<Real*>(v.base_d) = base_d;
+    Real c = 1, s = 0, ca = 1, sa = 0;
+    Real qa = src_local ? Real(1) : base_a;  // base_a^(0 + q0)
+    Real qd = dst_local ? Real(1) : base_d;
+    for (int m = 0; m < p_rot + 2; ++m) {
+        cbg[m * L] = c;
+        sbg[m * L] = s;
+        nsbg[m * L] = -s;
+        if (m < p_rot) {
+            cag[m * L] = ca;
+            sag[m * L] = sa;
+            qag[m * L] = qa;
+            qdg[m * L] = qd;
+        }
+        const Real nc = fma_(c, ang.cb, -(s * ang.sb));
+        const Real ns = fma_(s, ang.cb, c * ang.sb);
+        c = nc;
+        s = ns;
+        const Real nca = fma_(ca, ang.ca, -(sa * ang.sa));
+        const Real nsa = fma_(sa, ang.ca, ca * ang.sa);
+        ca = nca;
+        sa = nsa;
+        qa *= base_a;
+        qd *= base_d;
+    }
+}
+
+// Transposing butterfly over the 32 lanes: every lane enters with 32 values v[j]
+// (its own contribution to value index j) and lane l leaves with the sum over all
+// lanes of value index l in v[0]. 31 exchanges instead of 160; per value the
+// additions pair lanes at distance 16, 8, 4, 2, 1 (sharding.accumulation_tree).
+__device__ __forceinline__ void lane_transpose_sum(Real (&v)[32], int lane) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        const bool upper = lane & d;
+#pragma unroll
+        for (int j = 0; j < d; ++j) {
+            const Real send = upper ? v[j] : v[j + d];
+            const Real keep = upper ? v[j + d] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, d);
+        }
+    }
+}
 
 template <int TL>
 __global__ void __launch_bounds__(384, 1)
@@ -433,15 +561,9 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     Real* sm = reinterpret_cast<Real*>(smem_raw);
     Real* tab = sm;  // 16-byte aligned
     Real* buf = sm + lay.tab_len + lane;
-    Real* geo = sm + lay.tab_len + lay.buf_elems() + lane;  // ca1, sa1, rn, 1/rn
-    uint64_t* mbar =
-        reinterpret_cast<uint64_t*>(sm + lay.tab_len + lay.buf_elems() + lay.geo_elems());
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + lay.tab_len + lay.buf_elems());
     int* counters = reinterpret_cast<int*>(mbar + 1);
-    // per CTA: cos(m beta), sin(m beta), -sin(m beta), each [p_rot + 2][L] (two slack rows:
-    // the NCE code reads one class index past an odd-sized class)
-    Real* cbg = tt.beta + (size_t)blockIdx.x * 3 * (p_rot + 2) * L + lane;
-    Real* sbg = cbg + (size_t)(p_rot + 2) * L;
-    Real* nsbg = sbg + (size_t)(p_rot + 2) * L;
+    Real* geo_base = tt.scratch + (size_t)blockIdx.x * 2 * geo_elems<TL>(p_rot);
 
     const int kind = a.kind, p_in = a.p_in, p_out = a.p_out;
     const bool src_local = kind == KIND_L2L;
@@ -467,7 +589,11 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         a.phase_clocks[idx] += now - t_prev;                              \
         t_prev = now;                                                     \
     }
-    for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+    // geometry of the first group; later groups are prepared one group ahead, inside phase C
+    geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, src_local, dst_local, warp, lane);
+    int parity = 0;
+    for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x, parity ^= 1) {
+        const GeoView<TL> gv(geo_base + (size_t)parity * geo_elems<TL>(p_rot) + lane, p_rot);
         int64_t b[TL], src[TL];
         bool active[TL];
 #pragma unroll
@@ -481,119 +607,50 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
             }
             if (!active[t]) src[t] = 0;
         }
-
-        // ---- G: geometry tables (pipeline.cpp:52-91), one warp per slot set
-        if (warp < TL) {
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                if (t != warp) continue;
-                Real x = 0, y = 0, z = 1;
-                if (active[t]) {
-                    x = a.shifts[3 * b[t]];
-                    y = a.shifts[3 * b[t] + 1];
-                    z = a.shifts[3 * b[t] + 2];
-                }
-                const Angles<Real> ang = decompose_angles(x, y, z);
-                geo[0 * L + 32 * t] = ang.ca;
-                geo[1 * L + 32 * t] = ang.sa;
-                geo[2 * L + 32 * t] = ang.rn;
-                geo[3 * L + 32 * t] = Real(1) / ang.rn;
-                Real c = 1, s = 0;
-                for (int m = 0; m < p_rot + 2; ++m) {
-                    cbg[m * L + 32 * t] = c;
-                    sbg[m * L + 32 * t] = s;
-                    nsbg[m * L + 32 * t] = -s;
-                    const Real nc = fma_(c, ang.cb, -(s * ang.sb));
-                    const Real ns = fma_(s, ang.cb, c * ang.sb);
-                    c = nc;
-                    s = ns;
-                }
-            }
-        }
         if (threadIdx.x == 0) counters[0] = counters[1] = counters[2] = 0;
-        __syncthreads();
+        __syncthreads();  // geometry of this group (global scratch) and the counters are visible
         SFMM_PHASE_MARK(0)
 
-        // ---- A: load, rotate by +alpha, scale (pipeline.cpp:148-154); each warp
-        // takes an equal share of the column-major element list
-        {
-            const int T = p_in * (p_in + 1) / 2;
-            int e = (int)((long)T * warp / W);
-            const int e_end = (int)((long)T * (warp + 1) / W);
-            TriWalk w{0, 0, p_in};
-            {
-                int rem = e;
-                while (rem >= p_in - w.m) {
-                    rem -= p_in - w.m;
-                    ++w.m;
-                }
-                w.n = w.m + rem;
-            }
-            Real c1[TL], s1[TL], base[TL], c[TL], s[TL], qcol[TL], q[TL];
+        // ---- A: load, rotate by +alpha, scale (pipeline.cpp:148-154). One task per
+        // column m (all rows n >= m share e^{i m alpha}; the scale advances by one
+        // factor per row); warp w takes columns w, w + W, ... from the long end and
+        // the mirrored ones from the short end so that the shares are even.
+        for (int task = warp; task < p_in; task += W) {
+            const int m = (task & 1) ? p_in - 1 - (task >> 1) : (task >> 1);
+            Real c[TL], s[TL], q[TL], base[TL];
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
-                c1[t] = geo[0 * L + 32 * t];
-                s1[t] = geo[1 * L + 32 * t];
-                base[t] = src_local ? geo[2 * L + 32 * t] : geo[3 * L + 32 * t];
-                c[t] = 1;
-                s[t] = 0;
-                for (int j = 0; j < w.m; ++j) {
-                    const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));
-                    const Real ns = fma_(s[t], c1[t], c[t] * s1[t]);
-                    c[t] = nc;
-                    s[t] = ns;
-                }
-                // scale of element (n, m): |r|^n for local sources, |r|^-(n+1) otherwise,
-                // by repeated multiplication from 1 (pipeline.cpp:81-89)
-                qcol[t] = 1;
-                for (int j = 0; j < (src_local ? w.m : w.m + 1); ++j) qcol[t] *= base[t];
-                q[t] = qcol[t];
-                for (int j = w.m; j < w.n; ++j) q[t] *= base[t];
+                c[t] = __ldcg(gv.ca + m * L + 32 * t);
+                s[t] = __ldcg(gv.sa + m * L + 32 * t);
+                q[t] = __ldcg(gv.qa + m * L + 32 * t);
+                base[t] = __ldcg(gv.base_a + 32 * t);
             }
-            while (e < e_end) {
-                const int cnt = min(CH, e_end - e);
+            for (int n0 = m; n0 < p_in; n0 += CH) {
                 Real re[CH][TL], im[CH][TL];
-                TriWalk wl = w;
 #pragma unroll
                 for (int u = 0; u < CH; ++u) {
-                    if (u < cnt) {
-                        const int64_t off = (int64_t)aos_re(wl.n, wl.m) * a.in_stride;
+                    const int n = min(n0 + u, p_in - 1);
+                    const int64_t off = (int64_t)aos_re(n, m) * a.in_stride;
 #pragma unroll
-                        for (int t = 0; t < TL; ++t) {
-                            re[u][t] = active[t] ? a.in[off + src[t]] : Real(0);
-                            im[u][t] =
-                                (active[t] && wl.m) ? a.in[off + a.in_stride + src[t]] : Real(0);
-                        }
-                        wl.advance();
+                    for (int t = 0; t < TL; ++t) {
+                        re[u][t] = active[t] ? a.in[off + src[t]] : Real(0);
+                        im[u][t] = (active[t] && m) ? a.in[off + a.in_stride + src[t]] : Real(0);
                     }
                 }
 #pragma unroll
                 for (int u = 0; u < CH; ++u) {
-                    if (u < cnt) {
+                    const int n = n0 + u;
+                    if (n < p_in) {
 #pragma unroll
                         for (int t = 0; t < TL; ++t) {
                             const Real nr = q[t] * fma_(re[u][t], c[t], -(im[u][t] * s[t]));
                             const Real ni = q[t] * fma_(re[u][t], s[t], im[u][t] * c[t]);
-                            buf[t_re(w.n, w.m) * L + 32 * t] = nr;
-                            if (w.m) buf[t_im(w.n, w.m) * L + 32 * t] = ni;
+                            buf[t_re(n, m) * L + 32 * t] = nr;
+                            if (m) buf[t_im(n, m) * L + 32 * t] = ni;
                             q[t] *= base[t];
-                        }
-                        const int m_before = w.m;
-                        w.advance();
-                        if (w.m != m_before) {
-#pragma unroll
-                            for (int t = 0; t < TL; ++t) {
-                                const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));
-                                const Real ns = fma_(s[t], c1[t], c[t] * s1[t]);
-                                c[t] = nc;
-                                s[t] = ns;
-                                qcol[t] *= base[t];
-                                q[t] = qcol[t];
-                            }
                         }
                     }
                 }
-                e += cnt;
             }
         }
         if (tab_pending) {
@@ -606,7 +663,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
 
         // ---- B: forward swap passes, largest rows first
         {
-            Ctx<TL> c{(int)lay.tab_len, 0, cbg, sbg, src_local};
+            Ctx<TL> c{(int)lay.tab_len, 0, gv.cb, gv.sb, src_local};
             for (int task = fetch_task(&counters[0], lane); task < 2 * p_in;
                  task = fetch_task(&counters[0], lane)) {
                 const int n = p_in - 1 - (task >> 1);
@@ -636,9 +693,15 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         SFMM_PHASE_MARK(3)
 
         // ---- C: backward swap passes; columns >= cols of the z-step output are
-        // zero (pipeline.cpp:229-246) and are skipped, which is exact
+        // zero (pipeline.cpp:229-246) and are skipped, which is exact. The first
+        // TL warps prepare the geometry of the NEXT group before joining the queue:
+        // its serial recurrences hide behind the other warps' products.
         {
-            Ctx<TL> c{(int)lay.tab_len, 0, cbg, nsbg, dst_local};
+            if (g + gridDim.x < n_groups)
+                geometry_phase<TL>(a, g + gridDim.x, p_rot,
+                                   geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot), src_local,
+                                   dst_local, warp, lane);
+            Ctx<TL> c{(int)lay.tab_len, 0, gv.cb, gv.nsb, dst_local};
             for (int task = fetch_task(&counters[2], lane); task < 2 * p_out;
                  task = fetch_task(&counters[2], lane)) {
                 const int n = p_out - 1 - (task >> 1);
@@ -652,86 +715,64 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
             tab_pending = true;
         }
 
-        // ---- D: rotate by -alpha, scale (pipeline.cpp:251-257), store or reduce
-        {
-            const int T = p_out * (p_out + 1) / 2;
-            int e = (int)((long)T * warp / W);
-            const int e_end = (int)((long)T * (warp + 1) / W);
-            TriWalk w{0, 0, p_out};
-            {
-                int rem = e;
-                while (rem >= p_out - w.m) {
-                    rem -= p_out - w.m;
-                    ++w.m;
-                }
-                w.n = w.m + rem;
-            }
-            Real c1[TL], s1[TL], base[TL], c[TL], s[TL], qcol[TL], q[TL];
+        // ---- D: rotate by -alpha, scale (pipeline.cpp:251-257), store or reduce;
+        // column tasks as in phase A. In accumulate mode the 32*TL lanes of the
+        // group belong to one target: 16 rows of a column (32 values: re, im) are
+        // summed over the lanes with one transposing butterfly, slots l and l+32
+        // first (sharding.accumulation_tree restates the order).
+        for (int task = warp; task < p_out; task += W) {
+            const int m = (task & 1) ? p_out - 1 - (task >> 1) : (task >> 1);
+            Real c[TL], ms[TL], q[TL], base[TL];
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
-                c1[t] = geo[0 * L + 32 * t];
-                s1[t] = geo[1 * L + 32 * t];
-                base[t] = dst_local ? geo[3 * L + 32 * t] : geo[2 * L + 32 * t];
-                c[t] = 1;
-                s[t] = 0;
-                for (int j = 0; j < w.m; ++j) {
-                    const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));
-                    const Real ns = fma_(s[t], c1[t], c[t] * s1[t]);
-                    c[t] = nc;
-                    s[t] = ns;
-                }
-                // |r|^-n for local targets, |r|^(n+1) for multipole targets
-                qcol[t] = 1;
-                for (int j = 0; j < (dst_local ? w.m : w.m + 1); ++j) qcol[t] *= base[t];
-                q[t] = qcol[t];
-                for (int j = w.m; j < w.n; ++j) q[t] *= base[t];
+                c[t] = __ldcg(gv.ca + m * L + 32 * t);
+                ms[t] = -__ldcg(gv.sa + m * L + 32 * t);
+                q[t] = __ldcg(gv.qd + m * L + 32 * t);
+                base[t] = __ldcg(gv.base_d + 32 * t);
             }
-            for (; e < e_end; ++e) {
-                const int n = w.n, m = w.m;
-                Real nr[TL], ni[TL];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) {
-                    const Real re = buf[t_re(n, m) * L + 32 * t];
-                    const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
-                    const Real ms = -s[t];
-                    nr[t] = q[t] * fma_(re, c[t], -(im * ms));
-                    ni[t] = q[t] * fma_(re, ms, im * c[t]);
-                    q[t] *= base[t];
-                }
-                if (!accumulate) {
-#pragma unroll
-                    for (int t = 0; t < TL; ++t)
-                        if (active[t]) {
-                            a.out[(int64_t)aos_re(n, m) * a.out_stride + b[t]] = nr[t];
-                            a.out[(int64_t)(aos_re(n, m) + 1) * a.out_stride + b[t]] =
-                                m ? ni[t] : Real(0);
-                        }
-                } else {
-                    // fixed order: slots l and l+32 first, then the xor butterfly
-                    Real sr = nr[0], si = ni[0];
-#pragma unroll
-                    for (int t = 1; t < TL; ++t) {
-                        sr += nr[t];
-                        si += ni[t];
-                    }
-                    sr = warp_sum(sr);
-                    if (m) si = warp_sum(si);
-                    if (lane == 0) {
-                        a.out[(int64_t)aos_re(n, m) * a.out_stride + g] = sr;
-                        if (m) a.out[(int64_t)(aos_re(n, m) + 1) * a.out_stride + g] = si;
-                    }
-                }
-                w.advance();
-                if (w.m != m) {
+            if (!accumulate) {
+                for (int n = m; n < p_out; ++n) {
 #pragma unroll
                     for (int t = 0; t < TL; ++t) {
-                        const Real nc = fma_(c[t], c1[t], -(s[t] * s1[t]));
-                        const Real ns = fma_(s[t], c1[t], c[t] * s1[t]);
-                        c[t] = nc;
-                        s[t] = ns;
-                        qcol[t] *= base[t];
-                        q[t] = qcol[t];
+                        const Real re = buf[t_re(n, m) * L + 32 * t];
+                        const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
+                        const Real nr = q[t] * fma_(re, c[t], -(im * ms[t]));
+                        const Real ni = q[t] * fma_(re, ms[t], im * c[t]);
+                        q[t] *= base[t];
+                        if (active[t]) {
+                            a.out[(int64_t)aos_re(n, m) * a.out_stride + b[t]] = nr;
+                            a.out[(int64_t)(aos_re(n, m) + 1) * a.out_stride + b[t]] =
+                                m ? ni : Real(0);
+                        }
                     }
+                }
+            } else {
+                for (int n0 = m; n0 < p_out; n0 += 16) {
+                    Real v[32];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const int n = n0 + u;
+                        Real sr = 0, si = 0;
+                        if (n < p_out) {
+#pragma unroll
+                            for (int t = 0; t < TL; ++t) {
+                                const Real re = buf[t_re(n, m) * L + 32 * t];
+                                const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
+                                const Real nr = q[t] * fma_(re, c[t], -(im * ms[t]));
+                                const Real ni = q[t] * fma_(re, ms[t], im * c[t]);
+                                q[t] *= base[t];
+                                sr = t ? sr + nr : nr;
+                                si = t ? si + ni : ni;
+                            }
+                        }
+                        v[2 * u] = sr;
+                        v[2 * u + 1] = si;
+                    }
+                    lane_transpose_sum(v, lane);
+                    // lane l holds value index l: row n0 + (l >> 1), part l & 1
+                    const int n = n0 + (lane >> 1);
+                    if (n < p_out && !((lane & 1) && m == 0))
+                        a.out[(int64_t)(aos_re(n, m) + (lane & 1)) * a.out_stride + g] = v[0];
                 }
             }
         }
@@ -831,11 +872,11 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     tt.stream[1] = t.stream[1];
     tt.bytes[0] = (uint32_t)(staged(a.p_in) * sizeof(Real));
     tt.bytes[1] = (uint32_t)(staged(a.p_out) * sizeof(Real));
-    e = cudaMallocAsync((void**)&tt.beta, sizeof(Real) * (size_t)grid * 3 * (p_rot + 2) * L, stream);
+    e = cudaMallocAsync((void**)&tt.scratch, sizeof(Real) * (size_t)grid * 2 * geo_elems<TL>(p_rot), stream);
     if (e != cudaSuccess) return e;
     kern<<<grid, block, smem, stream>>>(a, tt, n_groups, p_rot, (int)tab_len);
     e = cudaGetLastError();
-    cudaFreeAsync(tt.beta, stream);
+    cudaFreeAsync(tt.scratch, stream);
     if (info) {
         info->grid = grid;
         info->block = block;
