@@ -708,6 +708,22 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
                 half_task_dispatch<TL>(c, n, task & 1, min(n, cols - 1));
             }
         }
+        // geometry of the columns this warp handles in phase D: the loads are in flight
+        // while the warp waits for the others at the barrier
+        Real dc[2][TL], dms[2][TL], dq[2][TL], dbase[TL];
+#pragma unroll
+        for (int ti = 0; ti < 2; ++ti) {
+            const int task = warp + ti * W;
+            const int m = task < p_out ? ((task & 1) ? p_out - 1 - (task >> 1) : (task >> 1)) : 0;
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                dc[ti][t] = __ldcg(gv.ca + m * L + 32 * t);
+                dms[ti][t] = -__ldcg(gv.sa + m * L + 32 * t);
+                dq[ti][t] = __ldcg(gv.qd + m * L + 32 * t);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < TL; ++t) dbase[t] = __ldcg(gv.base_d + 32 * t);
         __syncthreads();
         SFMM_PHASE_MARK(4)
         if (two_sides && g + gridDim.x < n_groups) {  // forward-side stream for the next group
@@ -720,15 +736,21 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         // group belong to one target: 16 rows of a column (32 values: re, im) are
         // summed over the lanes with one transposing butterfly, slots l and l+32
         // first (sharding.accumulation_tree restates the order).
-        for (int task = warp; task < p_out; task += W) {
+        for (int task = warp, ti = 0; task < p_out; task += W, ++ti) {
             const int m = (task & 1) ? p_out - 1 - (task >> 1) : (task >> 1);
             Real c[TL], ms[TL], q[TL], base[TL];
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
-                c[t] = __ldcg(gv.ca + m * L + 32 * t);
-                ms[t] = -__ldcg(gv.sa + m * L + 32 * t);
-                q[t] = __ldcg(gv.qd + m * L + 32 * t);
-                base[t] = __ldcg(gv.base_d + 32 * t);
+                base[t] = dbase[t];
+                if (ti < 2) {
+                    c[t] = dc[ti & 1][t];
+                    ms[t] = dms[ti & 1][t];
+                    q[t] = dq[ti & 1][t];
+                } else {
+                    c[t] = __ldcg(gv.ca + m * L + 32 * t);
+                    ms[t] = -__ldcg(gv.sa + m * L + 32 * t);
+                    q[t] = __ldcg(gv.qd + m * L + 32 * t);
+                }
             }
             if (!accumulate) {
                 for (int n = m; n < p_out; ++n) {

@@ -453,6 +453,15 @@ sfmm_status sfmm_create(sfmm_precision precision, int order, int device, int mu,
         return cuda_fail(e, "cudaGetDeviceProperties");
     }
     h->sm_count = prop.multiProcessorCount;
+    {
+        // per-call scratch comes from the stream-ordered pool: keep freed blocks cached
+        // instead of returning them to the driver at every synchronisation
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     sfmm_status st = precision == SFMM_F64 ? upload_tables<double>(h, h->td)
                                            : upload_tables<float>(h, h->tf);
     if (st == SFMM_OK) {
