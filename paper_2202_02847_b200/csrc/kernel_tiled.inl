@@ -589,76 +589,101 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         a.phase_clocks[idx] += now - t_prev;                              \
         t_prev = now;                                                     \
     }
-    // geometry of the first group; later groups are prepared one group ahead, inside phase C
+    // Column ownership of the elementwise phases: warp w owns columns from the long and
+    // the short end alternately (even shares). Phase D of group g and phase A of group
+    // g+1 touch column m only through its owner, so they run back to back per warp with
+    // no barrier in between, and the loads of the next group hide behind this one.
+    const int p_max = max(p_in, p_out);
+    // the ti-th column of this warp: (w, p_max-1-w), then (w+W, p_max-1-w-W), ... or -1
+    auto column_of = [&](int ti) {
+        const int k = warp + (ti >> 1) * W;       // pair index
+        if (2 * k >= p_max) return -1;
+        const int m = (ti & 1) ? p_max - 1 - k : k;
+        return ((ti & 1) && m == k) ? -1 : m;     // odd p_max: the middle column only once
+    };
+
+    // ---- A: load, rotate by +alpha, scale (pipeline.cpp:148-154), one column
+    auto phase_a_column = [&](int64_t ga, const GeoView<TL>& gva, int m) {
+        int64_t srca[TL];
+        bool acta[TL];
+#pragma unroll
+        for (int t = 0; t < TL; ++t) {
+            const int64_t bb = ga * L + 32 * t + lane;
+            srca[t] = bb;
+            acta[t] = bb < a.n;
+            if (acta[t] && accumulate) {
+                srca[t] = a.src_index[bb];
+                acta[t] = srca[t] >= 0;
+            }
+            if (!acta[t]) srca[t] = 0;
+        }
+        Real c[TL], s[TL], q[TL], base[TL];
+#pragma unroll
+        for (int t = 0; t < TL; ++t) {
+            c[t] = __ldcg(gva.ca + m * L + 32 * t);
+            s[t] = __ldcg(gva.sa + m * L + 32 * t);
+            q[t] = __ldcg(gva.qa + m * L + 32 * t);
+            base[t] = __ldcg(gva.base_a + 32 * t);
+        }
+        for (int n0 = m; n0 < p_in; n0 += CH) {
+            Real re[CH][TL], im[CH][TL];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const int n = min(n0 + u, p_in - 1);
+                const int64_t off = (int64_t)aos_re(n, m) * a.in_stride;
+#pragma unroll
+                for (int t = 0; t < TL; ++t) {
+                    re[u][t] = acta[t] ? a.in[off + srca[t]] : Real(0);
+                    im[u][t] = (acta[t] && m) ? a.in[off + a.in_stride + srca[t]] : Real(0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const int n = n0 + u;
+                if (n < p_in) {
+#pragma unroll
+                    for (int t = 0; t < TL; ++t) {
+                        const Real nr = q[t] * fma_(re[u][t], c[t], -(im[u][t] * s[t]));
+                        const Real ni = q[t] * fma_(re[u][t], s[t], im[u][t] * c[t]);
+                        buf[t_re(n, m) * L + 32 * t] = nr;
+                        if (m) buf[t_im(n, m) * L + 32 * t] = ni;
+                        q[t] *= base[t];
+                    }
+                }
+            }
+        }
+    };
+
+    // geometry and phase A of the first group; later groups are prepared one group
+    // ahead (geometry inside phase C, phase A fused behind phase D)
     geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, src_local, dst_local, warp, lane);
+    __syncthreads();
+    {
+        const GeoView<TL> gv0(geo_base + lane, p_rot);
+        for (int ti = 0; 2 * (warp + (ti >> 1) * W) < p_max; ++ti) {
+            const int m = column_of(ti);
+            if (m >= 0 && m < p_in) phase_a_column(blockIdx.x, gv0, m);
+        }
+    }
     int parity = 0;
     for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x, parity ^= 1) {
         const GeoView<TL> gv(geo_base + (size_t)parity * geo_elems<TL>(p_rot) + lane, p_rot);
-        int64_t b[TL], src[TL];
+        const GeoView<TL> gvn(geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot) + lane, p_rot);
+        const bool has_next = g + gridDim.x < n_groups;
+        int64_t b[TL];
         bool active[TL];
 #pragma unroll
         for (int t = 0; t < TL; ++t) {
             b[t] = g * L + 32 * t + lane;
-            src[t] = b[t];
             active[t] = b[t] < a.n;
-            if (active[t] && accumulate) {
-                src[t] = a.src_index[b[t]];
-                active[t] = src[t] >= 0;
-            }
-            if (!active[t]) src[t] = 0;
         }
         if (threadIdx.x == 0) counters[0] = counters[1] = counters[2] = 0;
-        __syncthreads();  // geometry of this group (global scratch) and the counters are visible
-        SFMM_PHASE_MARK(0)
-
-        // ---- A: load, rotate by +alpha, scale (pipeline.cpp:148-154). One task per
-        // column m (all rows n >= m share e^{i m alpha}; the scale advances by one
-        // factor per row); warp w takes columns w, w + W, ... from the long end and
-        // the mirrored ones from the short end so that the shares are even.
-        for (int task = warp; task < p_in; task += W) {
-            const int m = (task & 1) ? p_in - 1 - (task >> 1) : (task >> 1);
-            Real c[TL], s[TL], q[TL], base[TL];
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                c[t] = __ldcg(gv.ca + m * L + 32 * t);
-                s[t] = __ldcg(gv.sa + m * L + 32 * t);
-                q[t] = __ldcg(gv.qa + m * L + 32 * t);
-                base[t] = __ldcg(gv.base_a + 32 * t);
-            }
-            for (int n0 = m; n0 < p_in; n0 += CH) {
-                Real re[CH][TL], im[CH][TL];
-#pragma unroll
-                for (int u = 0; u < CH; ++u) {
-                    const int n = min(n0 + u, p_in - 1);
-                    const int64_t off = (int64_t)aos_re(n, m) * a.in_stride;
-#pragma unroll
-                    for (int t = 0; t < TL; ++t) {
-                        re[u][t] = active[t] ? a.in[off + src[t]] : Real(0);
-                        im[u][t] = (active[t] && m) ? a.in[off + a.in_stride + src[t]] : Real(0);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < CH; ++u) {
-                    const int n = n0 + u;
-                    if (n < p_in) {
-#pragma unroll
-                        for (int t = 0; t < TL; ++t) {
-                            const Real nr = q[t] * fma_(re[u][t], c[t], -(im[u][t] * s[t]));
-                            const Real ni = q[t] * fma_(re[u][t], s[t], im[u][t] * c[t]);
-                            buf[t_re(n, m) * L + 32 * t] = nr;
-                            if (m) buf[t_im(n, m) * L + 32 * t] = ni;
-                            q[t] *= base[t];
-                        }
-                    }
-                }
-            }
-        }
         if (tab_pending) {
             mbar_wait(mbar, tab_phase);
             tab_phase ^= 1;
             tab_pending = false;
         }
-        __syncthreads();
+        __syncthreads();  // phase A of this group, its operator stream and the counters are in place
         SFMM_PHASE_MARK(1)
 
         // ---- B: forward swap passes, largest rows first
@@ -697,7 +722,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         // TL warps prepare the geometry of the NEXT group before joining the queue:
         // its serial recurrences hide behind the other warps' products.
         {
-            if (g + gridDim.x < n_groups)
+            if (has_next)
                 geometry_phase<TL>(a, g + gridDim.x, p_rot,
                                    geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot), src_local,
                                    dst_local, warp, lane);
@@ -713,8 +738,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         Real dc[2][TL], dms[2][TL], dq[2][TL], dbase[TL];
 #pragma unroll
         for (int ti = 0; ti < 2; ++ti) {
-            const int task = warp + ti * W;
-            const int m = task < p_out ? ((task & 1) ? p_out - 1 - (task >> 1) : (task >> 1)) : 0;
+            const int m = min(max(column_of(ti), 0), p_out - 1);
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
                 dc[ti][t] = __ldcg(gv.ca + m * L + 32 * t);
@@ -726,79 +750,82 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         for (int t = 0; t < TL; ++t) dbase[t] = __ldcg(gv.base_d + 32 * t);
         __syncthreads();
         SFMM_PHASE_MARK(4)
-        if (two_sides && g + gridDim.x < n_groups) {  // forward-side stream for the next group
+        if (two_sides && has_next) {  // forward-side stream for the next group
             if (threadIdx.x == 0) bulk_load(tab, tt.stream[side_fwd], tt.bytes[0], mbar);
             tab_pending = true;
         }
 
-        // ---- D: rotate by -alpha, scale (pipeline.cpp:251-257), store or reduce;
-        // column tasks as in phase A. In accumulate mode the 32*TL lanes of the
-        // group belong to one target: 16 rows of a column (32 values: re, im) are
-        // summed over the lanes with one transposing butterfly, slots l and l+32
+        // ---- D: rotate by -alpha, scale (pipeline.cpp:251-257), store or reduce, then
+        // phase A of the next group on the same column. In accumulate mode the 32*TL
+        // lanes of the group belong to one target: 16 rows of a column (32 values: re,
+        // im) are summed over the lanes with one transposing butterfly, slots l and l+32
         // first (sharding.accumulation_tree restates the order).
-        for (int task = warp, ti = 0; task < p_out; task += W, ++ti) {
-            const int m = (task & 1) ? p_out - 1 - (task >> 1) : (task >> 1);
-            Real c[TL], ms[TL], q[TL], base[TL];
+        for (int ti = 0; 2 * (warp + (ti >> 1) * W) < p_max; ++ti) {
+            const int m = column_of(ti);
+            if (m < 0) continue;
+            if (m < p_out) {
+                Real c[TL], ms[TL], q[TL], base[TL];
 #pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                base[t] = dbase[t];
-                if (ti < 2) {
-                    c[t] = dc[ti & 1][t];
-                    ms[t] = dms[ti & 1][t];
-                    q[t] = dq[ti & 1][t];
-                } else {
-                    c[t] = __ldcg(gv.ca + m * L + 32 * t);
-                    ms[t] = -__ldcg(gv.sa + m * L + 32 * t);
-                    q[t] = __ldcg(gv.qd + m * L + 32 * t);
-                }
-            }
-            if (!accumulate) {
-                for (int n = m; n < p_out; ++n) {
-#pragma unroll
-                    for (int t = 0; t < TL; ++t) {
-                        const Real re = buf[t_re(n, m) * L + 32 * t];
-                        const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
-                        const Real nr = q[t] * fma_(re, c[t], -(im * ms[t]));
-                        const Real ni = q[t] * fma_(re, ms[t], im * c[t]);
-                        q[t] *= base[t];
-                        if (active[t]) {
-                            a.out[(int64_t)aos_re(n, m) * a.out_stride + b[t]] = nr;
-                            a.out[(int64_t)(aos_re(n, m) + 1) * a.out_stride + b[t]] =
-                                m ? ni : Real(0);
-                        }
+                for (int t = 0; t < TL; ++t) {
+                    base[t] = dbase[t];
+                    if (ti < 2) {
+                        c[t] = dc[ti & 1][t];
+                        ms[t] = dms[ti & 1][t];
+                        q[t] = dq[ti & 1][t];
+                    } else {
+                        c[t] = __ldcg(gv.ca + m * L + 32 * t);
+                        ms[t] = -__ldcg(gv.sa + m * L + 32 * t);
+                        q[t] = __ldcg(gv.qd + m * L + 32 * t);
                     }
                 }
-            } else {
-                for (int n0 = m; n0 < p_out; n0 += 16) {
-                    Real v[32];
+                if (!accumulate) {
+                    for (int n = m; n < p_out; ++n) {
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        const int n = n0 + u;
-                        Real sr = 0, si = 0;
-                        if (n < p_out) {
-#pragma unroll
-                            for (int t = 0; t < TL; ++t) {
-                                const Real re = buf[t_re(n, m) * L + 32 * t];
-                                const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
-                                const Real nr = q[t] * fma_(re, c[t], -(im * ms[t]));
-                                const Real ni = q[t] * fma_(re, ms[t], im * c[t]);
-                                q[t] *= base[t];
-                                sr = t ? sr + nr : nr;
-                                si = t ? si + ni : ni;
+                        for (int t = 0; t < TL; ++t) {
+                            const Real re = buf[t_re(n, m) * L + 32 * t];
+                            const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
+                            const Real nr = q[t] * fma_(re, c[t], -(im * ms[t]));
+                            const Real ni = q[t] * fma_(re, ms[t], im * c[t]);
+                            q[t] *= base[t];
+                            if (active[t]) {
+                                a.out[(int64_t)aos_re(n, m) * a.out_stride + b[t]] = nr;
+                                a.out[(int64_t)(aos_re(n, m) + 1) * a.out_stride + b[t]] =
+                                    m ? ni : Real(0);
                             }
                         }
-                        v[2 * u] = sr;
-                        v[2 * u + 1] = si;
                     }
-                    lane_transpose_sum(v, lane);
-                    // lane l holds value index l: row n0 + (l >> 1), part l & 1
-                    const int n = n0 + (lane >> 1);
-                    if (n < p_out && !((lane & 1) && m == 0))
-                        a.out[(int64_t)(aos_re(n, m) + (lane & 1)) * a.out_stride + g] = v[0];
+                } else {
+                    for (int n0 = m; n0 < p_out; n0 += 16) {
+                        Real v[32];
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const int n = n0 + u;
+                            Real sr = 0, si = 0;
+                            if (n < p_out) {
+#pragma unroll
+                                for (int t = 0; t < TL; ++t) {
+                                    const Real re = buf[t_re(n, m) * L + 32 * t];
+                                    const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
+                                    const Real nr = q[t] * fma_(re, c[t], -(im * ms[t]));
+                                    const Real ni = q[t] * fma_(re, ms[t], im * c[t]);
+                                    q[t] *= base[t];
+                                    sr = t ? sr + nr : nr;
+                                    si = t ? si + ni : ni;
+                                }
+                            }
+                            v[2 * u] = sr;
+                            v[2 * u + 1] = si;
+                        }
+                        lane_transpose_sum(v, lane);
+                        // lane l holds value index l: row n0 + (l >> 1), part l & 1
+                        const int n = n0 + (lane >> 1);
+                        if (n < p_out && !((lane & 1) && m == 0))
+                            a.out[(int64_t)(aos_re(n, m) + (lane & 1)) * a.out_stride + g] = v[0];
+                    }
                 }
             }
+            if (has_next && m < p_in) phase_a_column(g + gridDim.x, gvn, m);
         }
-        __syncthreads();
         SFMM_PHASE_MARK(5)
     }
 #undef SFMM_PHASE_MARK
