@@ -150,7 +150,10 @@ sfmm_status check_orders(const sfmm_handle* h, int kind, int p_in, int p_out) {
 // pipeline.cpp:296-297: norm(shift) < numeric_limits<Real>::min()
 template <typename Real>
 bool host_shift_degenerate(const Real* r) {
-    return std::hypot(r[0], r[1], r[2]) < std::numeric_limits<Real>::min();
+    // |r| >= max |component|: the norm needs evaluating only for all-subnormal shifts
+    const Real mn = std::numeric_limits<Real>::min();
+    if (std::fabs(r[0]) >= mn || std::fabs(r[1]) >= mn || std::fabs(r[2]) >= mn) return false;
+    return std::hypot(r[0], r[1], r[2]) < mn;
 }
 
 template <typename Real>
@@ -294,37 +297,59 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
         grp_ptr[(size_t)t + 1] = grp_ptr[(size_t)t] + (cnt + kPlanGroup - 1) / kPlanGroup;
     }
     const int64_t n_groups = grp_ptr[(size_t)n_targets];
-    std::vector<int32_t> si((size_t)n_groups * kPlanGroup, -1);
-    std::vector<Real> sh((size_t)n_groups * kPlanGroup * 3);
-    for (size_t i = 0; i < (size_t)n_groups * kPlanGroup; ++i) {
-        sh[3 * i] = 0;
-        sh[3 * i + 1] = 0;
-        sh[3 * i + 2] = 1;
-    }
-    for (int64_t t = 0; t < n_targets; ++t) {
-        int64_t dst = grp_ptr[(size_t)t] * kPlanGroup;
-        for (int64_t j = tgt_ptr[t]; j < tgt_ptr[t + 1]; ++j, ++dst) {
-            if (src_index[j] < 0 || src_index[j] >= n_sources)
-                return fail(SFMM_INVALID_ARGUMENT, "source index out of range");
-            if (host_shift_degenerate(shifts + 3 * j))
-                return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
-            si[(size_t)dst] = src_index[j];
-            std::memcpy(&sh[(size_t)(3 * dst)], shifts + 3 * j, sizeof(Real) * 3);
-        }
-    }
+    std::vector<int32_t> grp_target((size_t)std::max<int64_t>(n_groups, 1));
+    for (int64_t t = 0; t < n_targets; ++t)
+        for (int64_t g = grp_ptr[(size_t)t]; g < grp_ptr[(size_t)t + 1]; ++g)
+            grp_target[(size_t)g] = (int32_t)t;
     plan->h = h;
     plan->n_targets = n_targets;
     plan->n_pairs = n_pairs;
     plan->n_groups = n_groups;
     plan->n_sources = n_sources;
+    // the raw pair list goes to the device as it is; padding to whole groups and the
+    // validation (source range, zero shifts) happen there
+    cudaStream_t stream = nullptr;
+    const size_t padded = (size_t)std::max<int64_t>(n_groups, 1) * kPlanGroup;
     CU(cudaMalloc((void**)&plan->d_grp_ptr, sizeof(int64_t) * grp_ptr.size()));
-    CU(cudaMalloc((void**)&plan->d_src_index, sizeof(int32_t) * std::max<size_t>(si.size(), 1)));
-    CU(cudaMalloc(&plan->d_shifts, sizeof(Real) * std::max<size_t>(sh.size(), 1)));
-    CU(cudaMemcpy(plan->d_grp_ptr, grp_ptr.data(), sizeof(int64_t) * grp_ptr.size(),
-                  cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(plan->d_src_index, si.data(), sizeof(int32_t) * si.size(),
-                  cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(plan->d_shifts, sh.data(), sizeof(Real) * sh.size(), cudaMemcpyHostToDevice));
+    CU(cudaMalloc((void**)&plan->d_src_index, sizeof(int32_t) * padded));
+    CU(cudaMalloc(&plan->d_shifts, sizeof(Real) * padded * 3));
+    int64_t* d_tgt = nullptr;
+    int32_t *d_gt = nullptr, *d_idx = nullptr;
+    Real* d_sh = nullptr;
+    int* d_flags = nullptr;
+    const size_t np = (size_t)std::max<int64_t>(n_pairs, 1);
+    CU(cudaMallocAsync((void**)&d_tgt, sizeof(int64_t) * (n_targets + 1), stream));
+    CU(cudaMallocAsync((void**)&d_gt, sizeof(int32_t) * grp_target.size(), stream));
+    CU(cudaMallocAsync((void**)&d_idx, sizeof(int32_t) * np, stream));
+    CU(cudaMallocAsync((void**)&d_sh, sizeof(Real) * np * 3, stream));
+    CU(cudaMallocAsync((void**)&d_flags, sizeof(int) * 2, stream));
+    CU(cudaMemsetAsync(d_flags, 0, sizeof(int) * 2, stream));
+    CU(cudaMemcpyAsync(plan->d_grp_ptr, grp_ptr.data(), sizeof(int64_t) * grp_ptr.size(),
+                       cudaMemcpyHostToDevice, stream));
+    CU(cudaMemcpyAsync(d_tgt, tgt_ptr, sizeof(int64_t) * (n_targets + 1), cudaMemcpyHostToDevice,
+                       stream));
+    CU(cudaMemcpyAsync(d_gt, grp_target.data(), sizeof(int32_t) * grp_target.size(),
+                       cudaMemcpyHostToDevice, stream));
+    if (n_pairs > 0) {
+        CU(cudaMemcpyAsync(d_idx, src_index, sizeof(int32_t) * n_pairs, cudaMemcpyHostToDevice,
+                           stream));
+        CU(cudaMemcpyAsync(d_sh, shifts, sizeof(Real) * n_pairs * 3, cudaMemcpyHostToDevice,
+                           stream));
+    }
+    CU(launch_build_plan<Real>(d_tgt, plan->d_grp_ptr, d_gt, d_idx, d_sh, n_groups, n_sources,
+                               kPlanGroup, plan->d_src_index, static_cast<Real*>(plan->d_shifts),
+                               d_flags, stream));
+    h->launches += 1;
+    int flags[2] = {0, 0};
+    CU(cudaMemcpyAsync(flags, d_flags, sizeof(flags), cudaMemcpyDeviceToHost, stream));
+    cudaFreeAsync(d_tgt, stream);
+    cudaFreeAsync(d_gt, stream);
+    cudaFreeAsync(d_idx, stream);
+    cudaFreeAsync(d_sh, stream);
+    cudaFreeAsync(d_flags, stream);
+    CU(cudaStreamSynchronize(stream));
+    if (flags[0]) return fail(SFMM_INVALID_ARGUMENT, "source index out of range");
+    if (flags[1]) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
     return SFMM_OK;
 }
 

@@ -83,6 +83,14 @@ template <typename Real>
 cudaError_t launch_unpack_soa(const Real* soa, Real* aos, int64_t n, int p, int64_t stride,
                               cudaStream_t stream);
 
+// Accumulate mode, plan construction on the device (padding to groups + validation).
+template <typename Real>
+cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
+                              const int32_t* grp_target, const int32_t* src_index,
+                              const Real* shifts, int64_t n_groups, int64_t n_sources, int group,
+                              int32_t* out_index, Real* out_shifts, int* flags,
+                              cudaStream_t stream);
+
 // Accumulate mode, second stage: out[c][t] = sum_{g in groups of t} partial[c][g],
 // groups in ascending order. grp_ptr: [n_targets + 1] in units of `per` partial groups.
 template <typename Real>

@@ -51,6 +51,41 @@ __global__ void repack_kernel(const Real* __restrict__ src, Real* __restrict__ d
     }
 }
 
+// Accumulation plan: pads the pair list of every target to whole groups of 64 lanes
+// (idle lanes: source -1, benign shift (0,0,1)) and validates it on the way.
+// flags[0]: source index out of range, flags[1]: degenerate shift.
+template <typename Real>
+__global__ void build_plan_kernel(const int64_t* __restrict__ tgt_ptr,
+                                  const int64_t* __restrict__ grp_ptr,
+                                  const int32_t* __restrict__ grp_target,
+                                  const int32_t* __restrict__ src_index,
+                                  const Real* __restrict__ shifts, int64_t n_groups,
+                                  int64_t n_sources, int group, int32_t* __restrict__ out_index,
+                                  Real* __restrict__ out_shifts, int* flags) {
+    const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (d >= n_groups * group) return;
+    const int64_t g = d / group;
+    const int t = grp_target[g];
+    const int64_t j = tgt_ptr[t] + (g - grp_ptr[t]) * group + (d - g * group);
+    int32_t idx = -1;
+    Real x = 0, y = 0, z = 1;
+    if (j < tgt_ptr[t + 1]) {
+        idx = src_index[j];
+        x = shifts[3 * j];
+        y = shifts[3 * j + 1];
+        z = shifts[3 * j + 2];
+        if (idx < 0 || idx >= n_sources) {
+            flags[0] = 1;
+            idx = -1;
+        }
+        if (shift_is_degenerate(x, y, z)) flags[1] = 1;
+    }
+    out_index[d] = idx;
+    out_shifts[3 * d] = x;
+    out_shifts[3 * d + 1] = y;
+    out_shifts[3 * d + 2] = z;
+}
+
 template <typename Real>
 __global__ void reduce_groups_kernel(const Real* __restrict__ partial, int64_t n_groups,
                                      const int64_t* __restrict__ grp_ptr, int per,
@@ -163,6 +198,21 @@ cudaError_t launch_unpack_soa(const Real* soa, Real* aos, int64_t n, int p, int6
 }
 
 template <typename Real>
+cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
+                              const int32_t* grp_target, const int32_t* src_index,
+                              const Real* shifts, int64_t n_groups, int64_t n_sources, int group,
+                              int32_t* out_index, Real* out_shifts, int* flags,
+                              cudaStream_t stream) {
+    if (n_groups <= 0) return cudaSuccess;
+    const int block = 256;
+    const int64_t grid = (n_groups * group + block - 1) / block;
+    build_plan_kernel<Real><<<(unsigned)grid, block, 0, stream>>>(
+        tgt_ptr, grp_ptr, grp_target, src_index, shifts, n_groups, n_sources, group, out_index,
+        out_shifts, flags);
+    return cudaGetLastError();
+}
+
+template <typename Real>
 cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const int64_t* grp_ptr,
                                  int per, int64_t n_targets, int p_out, Real* out,
                                  int64_t out_stride, cudaStream_t stream) {
@@ -236,6 +286,9 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
     template cudaError_t launch_reduce_groups<Real>(const Real*, int64_t, const int64_t*, int,  \
                                                     int64_t, int, Real*, int64_t, cudaStream_t); \
     template int translate_group_size<Real>(const TranslateArgs<Real>&);                        \
+    template cudaError_t launch_build_plan<Real>(const int64_t*, const int64_t*, const int32_t*, \
+                                                 const int32_t*, const Real*, int64_t, int64_t, \
+                                                 int, int32_t*, Real*, int*, cudaStream_t);     \
     template cudaError_t launch_translate<Real>(const DeviceTables<Real>&,                      \
                                                 const TranslateArgs<Real>&, int, cudaStream_t,  \
                                                 LaunchInfo*);

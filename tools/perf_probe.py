@@ -61,5 +61,7 @@ if pc is not None:
     names = ["G geometry", "A load+rot", "B fwd swaps", "Z z-step", "C bwd swaps", "D rot+store"]
     print("phase cycles of CTA 0 (all launches):", ", ".join(f"{n}: {100*x/tot:.1f}%" for n, x in zip(names, v)), f"total {tot:.3e}")
 tps = units / (best * 1e-3)
-print(f"{mode} {kind} P={P} units={units} best_ms={best:.3f} translations/s={tps:.3e} "
+isz = 4 if prec == capi.F32 else 8
+gbs = tps * workloads.bytes_per_translation(P, P, isz) * 1e-9
+print(f"{mode} {kind} P={P} units={units} best_ms={best:.3f} translations/s={tps:.3e} algGB/s={gbs:.0f} "
       f"TFLOP/s={tps*flops*1e-12:.2f} of peak {peak:.1f} => frac={tps*flops*1e-12/peak:.3f}", flush=True)
