@@ -315,7 +315,11 @@ def main():
                     "path": "sfmm_plan_create + sfmm_m2l_accumulate_host from pageable host arrays"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
-                         "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                         # dram__bytes_read.sum + dram__bytes_write.sum of translate_tiled_kernel,
+                         # one ncu --set full capture of this workload at N=1
+                         # (profiles/ncu_full_translate_tiled_r01.csv)
+                         "traffic": 170.0e6 if world == 1 else None,
                          "peak_source": "sfmm_measure_fma_peak (DFMA, measured in this run); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
                          "flops_per_translation": flops},
