@@ -234,8 +234,8 @@ __device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax
         for (int i = 0; i < NCE; ++i)
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
-                const Real cm = __ldcg(cbp + 2 * i * L + 32 * t);
-                const Real s = __ldcg(sbp + 2 * i * L + 32 * t);
+                const Real cm = cbp[2 * i * L + 32 * t];
+                const Real s = sbp[2 * i * L + 32 * t];
                 const Real a = ure[i][t], b = uim[i][t];
                 ure[i][t] = fma_(a, cm, -(b * s));
                 uim[i][t] = fma_(a, s, b * cm);
@@ -416,8 +416,10 @@ struct TiledLayout {
     int p_rot;
     size_t tab_len;  // staged stream elements (prefix + TAB_PAD, multiple of 4)
     __host__ __device__ size_t buf_elems() const { return (size_t)p_rot * p_rot * L; }
+    // triangle, staged stream, {mbarrier, task counters} (32 bytes), cos/sin(alpha) of the
+    // current and the next group ([2][2][L])
     __host__ __device__ size_t smem_bytes() const {
-        return sizeof(Real) * (buf_elems() + tab_len) + 32;
+        return sizeof(Real) * (buf_elems() + tab_len + 4 * L) + 32;
     }
 };
 
@@ -431,6 +433,23 @@ struct TriWalk {
             n = m;
         }
     }
+};
+
+// element number e of the walk; e past the end gives n >= p, which every user skips
+__device__ __forceinline__ TriWalk tri_seek(int e, int p) {
+    int m = 0;
+    while (m < p && e >= p - m) {
+        e -= p - m;
+        ++m;
+    }
+    return TriWalk{m + e, m, p};
+}
+
+// Rotation and scale factors that travel with a TriWalk: cos/sin(m alpha) of the
+// current column, the scale q of the current row and qh of the column's first row.
+template <int TL>
+struct RotWalk {
+    Real c[TL], s[TL], q[TL], qh[TL], base[TL];
 };
 
 struct TiledTables {
@@ -474,8 +493,8 @@ struct GeoView {
 // all powers by repeated multiplication from 1 (pipeline.cpp:81-89).
 template <int TL>
 __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int64_t g, int p_rot,
-                                               Real* geo, bool src_local, bool dst_local, int warp,
-                                               int lane) {
+                                               Real* geo, Real* c1s1, bool src_local, bool dst_local,
+                                               int warp, int lane) {
     constexpr int L = 32 * TL;
     if (warp >= TL) return;
     const int t = warp;
@@ -502,6 +521,8 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
     const Real base_d = dst_local ? inv : ang.rn;
     *const_cast<Real*>(v.base_a) = base_a;
     *const_cast<Real*>(v.base_d) = base_d;
+    c1s1[32 * t + lane] = ang.ca;  // the step of the column recurrence in phases A and D
+    c1s1[L + 32 * t + lane] = ang.sa;
     Real c = 1, s = 0, ca = 1, sa = 0;
     Real qa = src_local ? Real(1) : base_a;  // base_a^(0 + q0)
     Real qd = dst_local ? Real(1) : base_d;
@@ -528,29 +549,251 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
     }
 }
 
-// Transposing butterfly over the 32 lanes: every lane enters with 32 values v[j]
-// (its own contribution to value index j) and lane l leaves with the sum over all
-// lanes of value index l in v[0]. 31 exchanges instead of 160; per value the
-// additions pair lanes at distance 16, 8, 4, 2, 1 (sharding.accumulation_tree).
-__device__ __forceinline__ void lane_transpose_sum(Real (&v)[32], int lane) {
+// Transposing butterfly over the 32 lanes: every lane enters with NV values v[j]
+// (its own contribution to value index j; NV = 8 or 16) and leaves with the sum over
+// all lanes of value index lane / (32 / NV) in v[0] (32 / NV neighbouring lanes hold
+// the same sum). NV exchanges instead of 5 NV; per value the additions pair lanes at
+// distance 16, 8, 4, 2, 1 (sharding.accumulation_tree).
+template <int NV>
+__device__ __forceinline__ void lane_transpose_sum(Real (&v)[NV], int lane) {
+    int d = 16;
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
+    for (int h = NV / 2; h >= 1; h >>= 1, d >>= 1) {
         const bool upper = lane & d;
 #pragma unroll
-        for (int j = 0; j < d; ++j) {
-            const Real send = upper ? v[j] : v[j + d];
-            const Real keep = upper ? v[j + d] : v[j];
+        for (int j = 0; j < h; ++j) {
+            const Real send = upper ? v[j] : v[j + h];
+            const Real keep = upper ? v[j + h] : v[j];
             v[j] = keep + __shfl_xor_sync(0xffffffffu, send, d);
         }
     }
+#pragma unroll
+    for (d = 16 / NV; d >= 1; d >>= 1) v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], d);
 }
+
+constexpr int CHK = 4;  // elements per chunk of the elementwise phases
+
+// Arguments of elementwise_phase (one call per warp and group).
+struct ElemArgs {
+    const Real* in;            // sources (SoA), in_stride between coefficients
+    int64_t in_stride;
+    Real* out;                 // outputs or per-group partial sums (SoA)
+    int64_t out_stride;
+    const int32_t* src_index;  // accumulate mode: source of every pair, else null
+    int64_t n;                 // translations of the launch
+    const Real* geo_d;         // geometry scratch of the group phase D finishes, or null
+    const Real* geo_a;         // geometry scratch of the group phase A loads, or null
+    int64_t g_d, g_a;          // their group numbers
+    int buf_off;               // element offsets into smem_raw: triangle,
+    int cs_d_off, cs_a_off;    //   cos/sin(alpha) rows of the two groups
+    int p_in, p_out, p_rot;
+    int c_lo, c_hi;            // chunks of this warp
+};
+
+// Phases D and A on the chunks of one warp (reference pipeline.cpp:251-257 and
+// :148-154). The triangle of order p_max is walked column by column (TriWalk) and cut
+// into chunks of CHK elements; a warp owns a contiguous run of chunks. Phase D of group
+// g and phase A of group g+1 touch an element only through its owner, so they run back
+// to back per chunk with no barrier in between: the global loads of the next group are
+// issued first and are in flight while the chunk of this group is rotated and reduced.
+// Out of line so that its registers are not shared with the long-lived state of the
+// kernel body.
+//   D: rotate by -alpha, scale, then store (ACC = false) or reduce over the group
+//      (ACC = true): the 32*TL lanes belong to one target, the 2 CHK values of a chunk
+//      (re, im per element) are summed over the lanes with one transposing butterfly,
+//      slots l and l+32 first (sharding.accumulation_tree restates the order).
+//   A: load, rotate by +alpha, scale.
+// The factors cos/sin(m alpha) and the scales are read from the geometry scratch at the
+// first element only and then follow the walk: next row = scale times base
+// (pipeline.cpp:81-89), next column = one step of the angle recurrence
+// (pipeline.cpp:70-79), the very operations that filled the tables.
+template <int TL, bool ACC>
+__device__ __noinline__ void elementwise_phase(const ElemArgs e) {
+    constexpr int L = 32 * TL;
+    const int lane = threadIdx.x & 31;
+    Real* sm = reinterpret_cast<Real*>(smem_raw);
+    Real* buf = sm + e.buf_off + lane;
+    const Real* csd = sm + e.cs_d_off + lane;
+    const Real* csa = sm + e.cs_a_off + lane;
+    const int p_in = e.p_in, p_out = e.p_out, p_rot = e.p_rot;
+    const int p_max = max(p_in, p_out);
+    const bool do_d = e.geo_d != nullptr, do_a = e.geo_a != nullptr;
+
+    auto rot_seek = [&](RotWalk<TL>& r, const TriWalk& w, const Real* ca, const Real* sa,
+                        const Real* qtab, const Real* basep) {
+        const int m = min(w.m, p_rot - 1), n = min(w.n, p_rot - 1);  // past the end: unused
+#pragma unroll
+        for (int t = 0; t < TL; ++t) {
+            r.c[t] = __ldcg(ca + m * L + 32 * t);
+            r.s[t] = __ldcg(sa + m * L + 32 * t);
+            r.qh[t] = __ldcg(qtab + m * L + 32 * t);
+            r.q[t] = __ldcg(qtab + n * L + 32 * t);
+            r.base[t] = __ldcg(basep + 32 * t);
+        }
+    };
+    auto rot_advance = [&](TriWalk& w, RotWalk<TL>& r, const Real* cs) {
+        ++w.n;
+#pragma unroll
+        for (int t = 0; t < TL; ++t) r.q[t] *= r.base[t];
+        if (w.n == w.p) {
+            ++w.m;
+            w.n = w.m;
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                const Real c1 = cs[32 * t], s1 = cs[L + 32 * t];
+                const Real nc = fma_(r.c[t], c1, -(r.s[t] * s1));
+                const Real ns = fma_(r.s[t], c1, r.c[t] * s1);
+                r.c[t] = nc;
+                r.s[t] = ns;
+                r.qh[t] *= r.base[t];
+                r.q[t] = r.qh[t];
+            }
+        }
+    };
+
+    TriWalk wd = tri_seek(CHK * e.c_lo, p_max), wa = wd;
+    RotWalk<TL> rd, ra;
+    int64_t bd[TL], srca[TL];
+    bool actd[TL], acta[TL];
+#pragma unroll
+    for (int t = 0; t < TL; ++t) {
+        bd[t] = e.g_d * L + 32 * t + lane;
+        actd[t] = do_d && bd[t] < e.n;
+        const int64_t bb = e.g_a * L + 32 * t + lane;
+        srca[t] = bb;
+        acta[t] = do_a && bb < e.n;
+        if (acta[t] && ACC) {
+            srca[t] = e.src_index[bb];
+            acta[t] = srca[t] >= 0;
+        }
+        if (!acta[t]) srca[t] = 0;
+    }
+    if (do_d) {
+        const GeoView<TL> gv(e.geo_d + lane, p_rot);
+        rot_seek(rd, wd, gv.ca, gv.sa, gv.qd, gv.base_d);
+    }
+    if (do_a) {
+        const GeoView<TL> gv(e.geo_a + lane, p_rot);
+        rot_seek(ra, wa, gv.ca, gv.sa, gv.qa, gv.base_a);
+    }
+
+    // ---- D on all chunks of the warp
+    if (do_d) {
+        for (int ci = e.c_lo; ci < e.c_hi; ++ci) {
+            if constexpr (!ACC) {
+#pragma unroll
+                for (int u = 0; u < CHK; ++u) {
+                    if (wd.n < p_out) {
+#pragma unroll
+                        for (int t = 0; t < TL; ++t) {
+                            const Real re = buf[t_re(wd.n, wd.m) * L + 32 * t];
+                            const Real im = wd.m ? buf[t_im(wd.n, wd.m) * L + 32 * t] : Real(0);
+                            const Real ms = -rd.s[t];
+                            const Real nr = rd.q[t] * fma_(re, rd.c[t], -(im * ms));
+                            const Real ni = rd.q[t] * fma_(re, ms, im * rd.c[t]);
+                            if (actd[t]) {
+                                const int64_t o = (int64_t)aos_re(wd.n, wd.m) * e.out_stride + bd[t];
+                                __stcg(e.out + o, nr);
+                                __stcg(e.out + o + e.out_stride, wd.m ? ni : Real(0));
+                            }
+                        }
+                    }
+                    rot_advance(wd, rd, csd);
+                }
+            } else {
+                constexpr int NV = 2 * CHK, REP = 32 / NV;
+                Real v[NV];
+                int my_n = p_out, my_m = 0;  // the element whose sum this lane stores
+#pragma unroll
+                for (int u = 0; u < CHK; ++u) {
+                    Real sr = 0, si = 0;
+                    if (wd.n < p_out) {
+#pragma unroll
+                        for (int t = 0; t < TL; ++t) {
+                            const Real re = buf[t_re(wd.n, wd.m) * L + 32 * t];
+                            const Real im = wd.m ? buf[t_im(wd.n, wd.m) * L + 32 * t] : Real(0);
+                            const Real ms = -rd.s[t];
+                            const Real nr = rd.q[t] * fma_(re, rd.c[t], -(im * ms));
+                            const Real ni = rd.q[t] * fma_(re, ms, im * rd.c[t]);
+                            sr = t ? sr + nr : nr;
+                            si = t ? si + ni : ni;
+                        }
+                    }
+                    v[2 * u] = sr;
+                    v[2 * u + 1] = si;
+                    if (lane / (2 * REP) == u) {
+                        my_n = wd.n;
+                        my_m = wd.m;
+                    }
+                    rot_advance(wd, rd, csd);
+                }
+                lane_transpose_sum<NV>(v, lane);
+                // lanes REP k .. REP k + REP-1 hold value k: element k >> 1, part k & 1
+                const int part = (lane / REP) & 1;
+                if (!(lane & (REP - 1)) && my_n < p_out && !(part && my_m == 0))
+                    __stcg(e.out + (int64_t)(aos_re(my_n, my_m) + part) * e.out_stride + e.g_d, v[0]);
+            }
+        }
+    }
+    if (!do_a) return;
+
+    // ---- A on the same chunks, two chunks of loads in flight. The addresses are always
+    // valid (clamped; idle slots read source 0) and the values are zeroed only when
+    // consumed, so that neither a branch nor a use stands between the loads.
+    TriWalk wl = wa;  // load cursor, runs ahead of wa
+    auto issue = [&](Real (&re)[CHK][TL], Real (&im)[CHK][TL]) {
+#pragma unroll
+        for (int u = 0; u < CHK; ++u) {
+            const int64_t off =
+                (int64_t)aos_re(min(wl.n, p_in - 1), min(wl.m, p_in - 1)) * e.in_stride;
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                re[u][t] = __ldcg(e.in + off + srca[t]);
+                im[u][t] = __ldcg(e.in + off + e.in_stride + srca[t]);
+            }
+            wl.advance();
+        }
+    };
+    auto finish = [&](const Real (&re)[CHK][TL], const Real (&im)[CHK][TL]) {
+#pragma unroll
+        for (int u = 0; u < CHK; ++u) {
+            if (wa.n < p_in) {
+#pragma unroll
+                for (int t = 0; t < TL; ++t) {
+                    const Real xr = acta[t] ? re[u][t] : Real(0);
+                    const Real xi = (acta[t] && wa.m) ? im[u][t] : Real(0);
+                    const Real nr = ra.q[t] * fma_(xr, ra.c[t], -(xi * ra.s[t]));
+                    const Real ni = ra.q[t] * fma_(xr, ra.s[t], xi * ra.c[t]);
+                    buf[t_re(wa.n, wa.m) * L + 32 * t] = nr;
+                    if (wa.m) buf[t_im(wa.n, wa.m) * L + 32 * t] = ni;
+                }
+            }
+            rot_advance(wa, ra, csa);
+        }
+    };
+    Real re0[CHK][TL], im0[CHK][TL], re1[CHK][TL], im1[CHK][TL];
+    if (e.c_lo < e.c_hi) issue(re0, im0);
+    for (int ci = e.c_lo; ci < e.c_hi; ci += 2) {
+        if (ci + 1 < e.c_hi) issue(re1, im1);
+        finish(re0, im0);
+        if (ci + 1 < e.c_hi) {
+            if (ci + 2 < e.c_hi) issue(re0, im0);
+            finish(re1, im1);
+        }
+    }
+}
+
+// The elementwise phase is entered through a pointer read at run time: an indirect call
+// uses the plain calling convention, which gives the callee its own registers (a direct
+// call makes ptxas fit caller and callee into one register budget and starves it).
+using ElemFn = void (*)(const ElemArgs);
+__device__ ElemFn g_elem_fn[2] = {elementwise_phase<2, false>, elementwise_phase<2, true>};
 
 template <int TL>
 __global__ void __launch_bounds__(384, 1)
 translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, int p_rot,
                        int tab_len) {
     constexpr int L = 32 * TL;
-    constexpr int CH = 4;  // elements whose global loads are issued together
     if (a.fail_flag && *a.fail_flag) return;
 
     const int lane = threadIdx.x & 31;
@@ -589,82 +832,36 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         a.phase_clocks[idx] += now - t_prev;                              \
         t_prev = now;                                                     \
     }
-    // Column ownership of the elementwise phases: warp w owns columns from the long and
-    // the short end alternately (even shares). Phase D of group g and phase A of group
-    // g+1 touch column m only through its owner, so they run back to back per warp with
-    // no barrier in between, and the loads of the next group hide behind this one.
+    // elementwise phases (elementwise_phase): warp w owns a contiguous run of chunks
     const int p_max = max(p_in, p_out);
-    // the ti-th column of this warp: (w, p_max-1-w), then (w+W, p_max-1-w-W), ... or -1
-    auto column_of = [&](int ti) {
-        const int k = warp + (ti >> 1) * W;       // pair index
-        if (2 * k >= p_max) return -1;
-        const int m = (ti & 1) ? p_max - 1 - k : k;
-        return ((ti & 1) && m == k) ? -1 : m;     // odd p_max: the middle column only once
-    };
-
-    // ---- A: load, rotate by +alpha, scale (pipeline.cpp:148-154), one column
-    auto phase_a_column = [&](int64_t ga, const GeoView<TL>& gva, int m) {
-        int64_t srca[TL];
-        bool acta[TL];
-#pragma unroll
-        for (int t = 0; t < TL; ++t) {
-            const int64_t bb = ga * L + 32 * t + lane;
-            srca[t] = bb;
-            acta[t] = bb < a.n;
-            if (acta[t] && accumulate) {
-                srca[t] = a.src_index[bb];
-                acta[t] = srca[t] >= 0;
-            }
-            if (!acta[t]) srca[t] = 0;
-        }
-        Real c[TL], s[TL], q[TL], base[TL];
-#pragma unroll
-        for (int t = 0; t < TL; ++t) {
-            c[t] = __ldcg(gva.ca + m * L + 32 * t);
-            s[t] = __ldcg(gva.sa + m * L + 32 * t);
-            q[t] = __ldcg(gva.qa + m * L + 32 * t);
-            base[t] = __ldcg(gva.base_a + 32 * t);
-        }
-        for (int n0 = m; n0 < p_in; n0 += CH) {
-            Real re[CH][TL], im[CH][TL];
-#pragma unroll
-            for (int u = 0; u < CH; ++u) {
-                const int n = min(n0 + u, p_in - 1);
-                const int64_t off = (int64_t)aos_re(n, m) * a.in_stride;
-#pragma unroll
-                for (int t = 0; t < TL; ++t) {
-                    re[u][t] = acta[t] ? a.in[off + srca[t]] : Real(0);
-                    im[u][t] = (acta[t] && m) ? a.in[off + a.in_stride + srca[t]] : Real(0);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < CH; ++u) {
-                const int n = n0 + u;
-                if (n < p_in) {
-#pragma unroll
-                    for (int t = 0; t < TL; ++t) {
-                        const Real nr = q[t] * fma_(re[u][t], c[t], -(im[u][t] * s[t]));
-                        const Real ni = q[t] * fma_(re[u][t], s[t], im[u][t] * c[t]);
-                        buf[t_re(n, m) * L + 32 * t] = nr;
-                        if (m) buf[t_im(n, m) * L + 32 * t] = ni;
-                        q[t] *= base[t];
-                    }
-                }
-            }
-        }
-    };
+    const int n_chunks = (p_max * (p_max + 1) / 2 + CHK - 1) / CHK;
+    const int cs_off = (int)(lay.tab_len + lay.buf_elems()) + 32 / (int)sizeof(Real);
+    Real* c1s1 = sm + cs_off;  // [2 groups][cos alpha | sin alpha][L]
+    ElemArgs ea;
+    ea.in = a.in;
+    ea.in_stride = a.in_stride;
+    ea.out = a.out;
+    ea.out_stride = a.out_stride;
+    ea.src_index = a.src_index;
+    ea.n = a.n;
+    ea.buf_off = (int)lay.tab_len;
+    ea.p_in = p_in;
+    ea.p_out = p_out;
+    ea.p_rot = p_rot;
+    ea.c_lo = n_chunks * warp / W;
+    ea.c_hi = n_chunks * (warp + 1) / W;
 
     // geometry and phase A of the first group; later groups are prepared one group
     // ahead (geometry inside phase C, phase A fused behind phase D)
-    geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, src_local, dst_local, warp, lane);
+    geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, c1s1, src_local, dst_local, warp, lane);
     __syncthreads();
-    {
-        const GeoView<TL> gv0(geo_base + lane, p_rot);
-        for (int ti = 0; 2 * (warp + (ti >> 1) * W) < p_max; ++ti) {
-            const int m = column_of(ti);
-            if (m >= 0 && m < p_in) phase_a_column(blockIdx.x, gv0, m);
-        }
-    }
+    ea.geo_d = nullptr;
+    ea.geo_a = geo_base;
+    ea.g_d = 0;
+    ea.g_a = blockIdx.x;
+    ea.cs_d_off = ea.cs_a_off = cs_off;
+    const ElemFn elem_fn = g_elem_fn[accumulate ? 1 : 0];
+    elem_fn(ea);
     int parity = 0;
     for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x, parity ^= 1) {
         const GeoView<TL> gv(geo_base + (size_t)parity * geo_elems<TL>(p_rot) + lane, p_rot);
@@ -724,8 +921,8 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         {
             if (has_next)
                 geometry_phase<TL>(a, g + gridDim.x, p_rot,
-                                   geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot), src_local,
-                                   dst_local, warp, lane);
+                                   geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot),
+                                   c1s1 + (parity ^ 1) * 2 * L, src_local, dst_local, warp, lane);
             Ctx<TL> c{(int)lay.tab_len, 0, gv.cb, gv.nsb, dst_local};
             for (int task = fetch_task(&counters[2], lane); task < 2 * p_out;
                  task = fetch_task(&counters[2], lane)) {
@@ -733,21 +930,6 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
                 half_task_dispatch<TL>(c, n, task & 1, min(n, cols - 1));
             }
         }
-        // geometry of the columns this warp handles in phase D: the loads are in flight
-        // while the warp waits for the others at the barrier
-        Real dc[2][TL], dms[2][TL], dq[2][TL], dbase[TL];
-#pragma unroll
-        for (int ti = 0; ti < 2; ++ti) {
-            const int m = min(max(column_of(ti), 0), p_out - 1);
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                dc[ti][t] = __ldcg(gv.ca + m * L + 32 * t);
-                dms[ti][t] = -__ldcg(gv.sa + m * L + 32 * t);
-                dq[ti][t] = __ldcg(gv.qd + m * L + 32 * t);
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < TL; ++t) dbase[t] = __ldcg(gv.base_d + 32 * t);
         __syncthreads();
         SFMM_PHASE_MARK(4)
         if (two_sides && has_next) {  // forward-side stream for the next group
@@ -755,77 +937,14 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
             tab_pending = true;
         }
 
-        // ---- D: rotate by -alpha, scale (pipeline.cpp:251-257), store or reduce, then
-        // phase A of the next group on the same column. In accumulate mode the 32*TL
-        // lanes of the group belong to one target: 16 rows of a column (32 values: re,
-        // im) are summed over the lanes with one transposing butterfly, slots l and l+32
-        // first (sharding.accumulation_tree restates the order).
-        for (int ti = 0; 2 * (warp + (ti >> 1) * W) < p_max; ++ti) {
-            const int m = column_of(ti);
-            if (m < 0) continue;
-            if (m < p_out) {
-                Real c[TL], ms[TL], q[TL], base[TL];
-#pragma unroll
-                for (int t = 0; t < TL; ++t) {
-                    base[t] = dbase[t];
-                    if (ti < 2) {
-                        c[t] = dc[ti & 1][t];
-                        ms[t] = dms[ti & 1][t];
-                        q[t] = dq[ti & 1][t];
-                    } else {
-                        c[t] = __ldcg(gv.ca + m * L + 32 * t);
-                        ms[t] = -__ldcg(gv.sa + m * L + 32 * t);
-                        q[t] = __ldcg(gv.qd + m * L + 32 * t);
-                    }
-                }
-                if (!accumulate) {
-                    for (int n = m; n < p_out; ++n) {
-#pragma unroll
-                        for (int t = 0; t < TL; ++t) {
-                            const Real re = buf[t_re(n, m) * L + 32 * t];
-                            const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
-                            const Real nr = q[t] * fma_(re, c[t], -(im * ms[t]));
-                            const Real ni = q[t] * fma_(re, ms[t], im * c[t]);
-                            q[t] *= base[t];
-                            if (active[t]) {
-                                a.out[(int64_t)aos_re(n, m) * a.out_stride + b[t]] = nr;
-                                a.out[(int64_t)(aos_re(n, m) + 1) * a.out_stride + b[t]] =
-                                    m ? ni : Real(0);
-                            }
-                        }
-                    }
-                } else {
-                    for (int n0 = m; n0 < p_out; n0 += 16) {
-                        Real v[32];
-#pragma unroll
-                        for (int u = 0; u < 16; ++u) {
-                            const int n = n0 + u;
-                            Real sr = 0, si = 0;
-                            if (n < p_out) {
-#pragma unroll
-                                for (int t = 0; t < TL; ++t) {
-                                    const Real re = buf[t_re(n, m) * L + 32 * t];
-                                    const Real im = m ? buf[t_im(n, m) * L + 32 * t] : Real(0);
-                                    const Real nr = q[t] * fma_(re, c[t], -(im * ms[t]));
-                                    const Real ni = q[t] * fma_(re, ms[t], im * c[t]);
-                                    q[t] *= base[t];
-                                    sr = t ? sr + nr : nr;
-                                    si = t ? si + ni : ni;
-                                }
-                            }
-                            v[2 * u] = sr;
-                            v[2 * u + 1] = si;
-                        }
-                        lane_transpose_sum(v, lane);
-                        // lane l holds value index l: row n0 + (l >> 1), part l & 1
-                        const int n = n0 + (lane >> 1);
-                        if (n < p_out && !((lane & 1) && m == 0))
-                            a.out[(int64_t)(aos_re(n, m) + (lane & 1)) * a.out_stride + g] = v[0];
-                    }
-                }
-            }
-            if (has_next && m < p_in) phase_a_column(g + gridDim.x, gvn, m);
-        }
+        // ---- D of this group, A of the next one
+        ea.geo_d = geo_base + (size_t)parity * geo_elems<TL>(p_rot);
+        ea.geo_a = has_next ? geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot) : nullptr;
+        ea.g_d = g;
+        ea.g_a = g + gridDim.x;
+        ea.cs_d_off = cs_off + parity * 2 * L;
+        ea.cs_a_off = cs_off + (parity ^ 1) * 2 * L;
+        elem_fn(ea);
         SFMM_PHASE_MARK(5)
     }
 #undef SFMM_PHASE_MARK

@@ -59,6 +59,7 @@ h.stream_status(stream)
 if pc is not None:
     v = pc.cpu().numpy().astype(float); tot = v.sum()
     names = ["G geometry", "A load+rot", "B fwd swaps", "Z z-step", "C bwd swaps", "D rot+store"]
+    print("raw", [int(x) for x in v])
     print("phase cycles of CTA 0 (all launches):", ", ".join(f"{n}: {100*x/tot:.1f}%" for n, x in zip(names, v)), f"total {tot:.3e}")
 tps = units / (best * 1e-3)
 isz = 4 if prec == capi.F32 else 8
