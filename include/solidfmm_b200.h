@@ -119,6 +119,15 @@ sfmm_status sfmm_pack_soa(sfmm_handle* h, int64_t n, int p, const void* d_aos,
 sfmm_status sfmm_unpack_soa(sfmm_handle* h, int64_t n, int p, const void* d_soa,
                             int64_t stride, void* d_aos, void* stream);
 
+/* "Rows" layout for expansions that are GATHERED by index (the sources of
+ * sfmm_m2l_accumulate_rows): expansion-major like the reference
+ * (solid.hpp:59-70: row n holds re, im of m = 0..n), with every row padded to a
+ * multiple of four values so that a thread that fetches its own source reads
+ * whole 32-byte sectors. sfmm_rows_len(p) values per expansion. */
+int64_t sfmm_rows_len(int p);
+sfmm_status sfmm_pack_rows(sfmm_handle* h, int64_t n, int p, const void* d_aos,
+                           void* d_rows, void* stream);
+
 /* ---- target-owned M2L accumulation (a full interaction-list level) -------
  * L[t] = sum over the sources s of target t of m2l(M[s], shift(t, s)), each
  * term computed exactly as the batched call computes it, summed without
@@ -143,6 +152,13 @@ int64_t sfmm_plan_pairs(const sfmm_plan* plan);
 sfmm_status sfmm_m2l_accumulate(sfmm_handle* h, const sfmm_plan* plan, int p_in,
                                 int p_out, const void* d_src, int64_t src_stride,
                                 void* d_out, int64_t out_stride, void* stream);
+
+/* The same with the sources in the rows layout, [n_sources][sfmm_rows_len(p_in)]:
+ * the faster form, the gather of a source costs a quarter of the memory
+ * transactions of the SoA form. Results are bit-identical. */
+sfmm_status sfmm_m2l_accumulate_rows(sfmm_handle* h, const sfmm_plan* plan, int p_in,
+                                     int p_out, const void* d_src_rows, void* d_out,
+                                     int64_t out_stride, void* stream);
 
 /* Host AoS form of the same: sources [n_sources][P_in(P_in+1)], outputs
  * [n_targets][P_out(P_out+1)], copies inside the call. */

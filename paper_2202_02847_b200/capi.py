@@ -43,6 +43,10 @@ _SIGNATURES = {
     "sfmm_stream_status": (c_int, [c_void_p, c_void_p]),
     "sfmm_pack_soa": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int64, c_void_p]),
     "sfmm_unpack_soa": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_int64, c_void_p, c_void_p]),
+    "sfmm_rows_len": (c_int64, [c_int]),
+    "sfmm_pack_rows": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p]),
+    "sfmm_m2l_accumulate_rows": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p,
+                                         c_int64, c_void_p]),
     "sfmm_plan_create": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
                                  POINTER(c_void_p)]),
     "sfmm_plan_destroy": (None, [c_void_p]),
@@ -248,6 +252,12 @@ class Handle:
         check(self._lib.sfmm_unpack_soa(self._h, n, p, _ptr(d_soa), stride, _ptr(d_aos),
                                         _ptr(stream)))
 
+    def rows_len(self, p: int) -> int:
+        return int(self._lib.sfmm_rows_len(p))
+
+    def pack_rows(self, n: int, p: int, d_aos, d_rows, stream=None) -> None:
+        check(self._lib.sfmm_pack_rows(self._h, n, p, _ptr(d_aos), _ptr(d_rows), _ptr(stream)))
+
     # -- target-owned accumulation -----------------------------------------
     def plan(self, tgt_ptr, src_index, shifts, n_sources: int) -> "Plan":
         return Plan(self, tgt_ptr, src_index, shifts, n_sources)
@@ -286,6 +296,12 @@ class Plan:
                    stream=None) -> None:
         check(self._lib.sfmm_m2l_accumulate(self._handle._h, self._p, p_in, p_out, _ptr(d_src),
                                             src_stride, _ptr(d_out), out_stride, _ptr(stream)))
+
+    def accumulate_rows(self, p_in: int, p_out: int, d_src_rows, d_out, out_stride: int,
+                        stream=None) -> None:
+        check(self._lib.sfmm_m2l_accumulate_rows(self._handle._h, self._p, p_in, p_out,
+                                                 _ptr(d_src_rows), _ptr(d_out), out_stride,
+                                                 _ptr(stream)))
 
     def accumulate_host(self, p_in: int, p_out: int, src: np.ndarray,
                         out: np.ndarray | None = None) -> np.ndarray:

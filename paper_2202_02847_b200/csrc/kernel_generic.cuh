@@ -260,8 +260,14 @@ translate_generic_kernel(DeviceTables<Real> t, TranslateArgs<Real> a, Real* gscr
                 for (int n = m; n < p_in; ++n) {
                     Real re = 0, im = 0;
                     if (active) {
-                        re = a.in[(int64_t)aos_re(n, m) * a.in_stride + src];
-                        if (m) im = a.in[(int64_t)(aos_re(n, m) + 1) * a.in_stride + src];
+                        if (a.in_layout == LAYOUT_ROWS) {
+                            const Real* row = a.in + src * a.in_stride + rows_off(n) + 2 * m;
+                            re = row[0];
+                            if (m) im = row[1];
+                        } else {
+                            re = a.in[(int64_t)aos_re(n, m) * a.in_stride + src];
+                            if (m) im = a.in[(int64_t)(aos_re(n, m) + 1) * a.in_stride + src];
+                        }
                     }
                     const Real sc = src_local ? pw[n * kLanes] : ipw[(n + 1) * kLanes];
                     const Real nr = sc * fma_(re, c, -(im * s));

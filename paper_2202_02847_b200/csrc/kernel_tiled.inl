@@ -416,40 +416,11 @@ struct TiledLayout {
     int p_rot;
     size_t tab_len;  // staged stream elements (prefix + TAB_PAD, multiple of 4)
     __host__ __device__ size_t buf_elems() const { return (size_t)p_rot * p_rot * L; }
-    // triangle, staged stream, {mbarrier, task counters} (32 bytes), cos/sin(alpha) of the
-    // current and the next group ([2][2][L])
+    // triangle, staged stream, {mbarrier, 4 task counters} (32 bytes), per-row completion
+    // counters of the backward swap pass
     __host__ __device__ size_t smem_bytes() const {
-        return sizeof(Real) * (buf_elems() + tab_len + 4 * L) + 32;
+        return sizeof(Real) * (buf_elems() + tab_len) + 32 + sizeof(int) * ((PMAX + 3) / 4 * 4);
     }
-};
-
-// Column-major walk over the triangle (n, m), n >= m, of order p: the element
-// order of phases A and D.
-struct TriWalk {
-    int n, m, p;
-    __device__ __forceinline__ void advance() {
-        if (++n == p) {
-            ++m;
-            n = m;
-        }
-    }
-};
-
-// element number e of the walk; e past the end gives n >= p, which every user skips
-__device__ __forceinline__ TriWalk tri_seek(int e, int p) {
-    int m = 0;
-    while (m < p && e >= p - m) {
-        e -= p - m;
-        ++m;
-    }
-    return TriWalk{m + e, m, p};
-}
-
-// Rotation and scale factors that travel with a TriWalk: cos/sin(m alpha) of the
-// current column, the scale q of the current row and qh of the column's first row.
-template <int TL>
-struct RotWalk {
-    Real c[TL], s[TL], q[TL], qh[TL], base[TL];
 };
 
 struct TiledTables {
@@ -493,8 +464,8 @@ struct GeoView {
 // all powers by repeated multiplication from 1 (pipeline.cpp:81-89).
 template <int TL>
 __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int64_t g, int p_rot,
-                                               Real* geo, Real* c1s1, bool src_local, bool dst_local,
-                                               int warp, int lane) {
+                                               Real* geo, bool src_local, bool dst_local, int warp,
+                                               int lane) {
     constexpr int L = 32 * TL;
     if (warp >= TL) return;
     const int t = warp;
@@ -521,8 +492,6 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
     const Real base_d = dst_local ? inv : ang.rn;
     *const_cast<Real*>(v.base_a) = base_a;
     *const_cast<Real*>(v.base_d) = base_d;
-    c1s1[32 * t + lane] = ang.ca;  // the step of the column recurrence in phases A and D
-    c1s1[L + 32 * t + lane] = ang.sa;
     Real c = 1, s = 0, ca = 1, sa = 0;
     Real qa = src_local ? Real(1) : base_a;  // base_a^(0 + q0)
     Real qd = dst_local ? Real(1) : base_d;
@@ -571,229 +540,251 @@ __device__ __forceinline__ void lane_transpose_sum(Real (&v)[NV], int lane) {
     for (d = 16 / NV; d >= 1; d >>= 1) v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], d);
 }
 
-constexpr int CHK = 4;  // elements per chunk of the elementwise phases
+constexpr int CHK = 4;  // elements per butterfly of phase D
 
-// Arguments of elementwise_phase (one call per warp and group).
-struct ElemArgs {
-    const Real* in;            // sources (SoA), in_stride between coefficients
-    int64_t in_stride;
+__device__ __forceinline__ int ld_volatile_shared(const int* p) {
+    return *reinterpret_cast<const volatile int*>(p);
+}
+
+// Arguments of elementwise_rows (one call per warp and phase).
+struct RowArgs {
+    const Real* in;            // sources: SoA (in_stride between coefficients) or rows
+    int64_t in_stride;         //          (in_stride between expansions), see ROWS below
     Real* out;                 // outputs or per-group partial sums (SoA)
     int64_t out_stride;
     const int32_t* src_index;  // accumulate mode: source of every pair, else null
-    int64_t n;                 // translations of the launch
+    int64_t n_total;           // translations of the launch
     const Real* geo_d;         // geometry scratch of the group phase D finishes, or null
     const Real* geo_a;         // geometry scratch of the group phase A loads, or null
     int64_t g_d, g_a;          // their group numbers
-    int buf_off;               // element offsets into smem_raw: triangle,
-    int cs_d_off, cs_a_off;    //   cos/sin(alpha) rows of the two groups
+    int buf_off;               // element offset of the triangle in smem_raw
+    int misc_off;              // byte offset of {mbarrier, counters, row_done} in smem_raw
     int p_in, p_out, p_rot;
-    int c_lo, c_hi;            // chunks of this warp
+    int gen;                   // groups this CTA has started: row_done[n] == 2 gen when row n is ready
 };
 
-// Phases D and A on the chunks of one warp (reference pipeline.cpp:251-257 and
-// :148-154). The triangle of order p_max is walked column by column (TriWalk) and cut
-// into chunks of CHK elements; a warp owns a contiguous run of chunks. Phase D of group
-// g and phase A of group g+1 touch an element only through its owner, so they run back
-// to back per chunk with no barrier in between: the global loads of the next group are
-// issued first and are in flight while the chunk of this group is rotated and reduced.
-// Out of line so that its registers are not shared with the long-lived state of the
-// kernel body.
-//   D: rotate by -alpha, scale, then store (ACC = false) or reduce over the group
-//      (ACC = true): the 32*TL lanes belong to one target, the 2 CHK values of a chunk
-//      (re, im per element) are summed over the lanes with one transposing butterfly,
-//      slots l and l+32 first (sharding.accumulation_tree restates the order).
-//   A: load, rotate by +alpha, scale.
-// The factors cos/sin(m alpha) and the scales are read from the geometry scratch at the
-// first element only and then follow the walk: next row = scale times base
-// (pipeline.cpp:81-89), next column = one step of the angle recurrence
-// (pipeline.cpp:70-79), the very operations that filled the tables.
-template <int TL, bool ACC>
-__device__ __noinline__ void elementwise_phase(const ElemArgs e) {
+// Phases D and A, row by row (reference pipeline.cpp:251-257 and :148-154):
+//   D (group g):   rotate by -alpha, scale by the row factor, then store (ACC = false)
+//                  or reduce over the group (ACC = true): the 32*TL lanes belong to one
+//                  target; the 2 CHK values of CHK elements (re, im) are summed over the
+//                  lanes with one transposing butterfly, slots l and l+32 first
+//                  (sharding.accumulation_tree restates the order);
+//   A (group g+1): load, rotate by +alpha, scale, into the places D has just read.
+// Both touch row n only, like the backward swap pass before them, so a row waits for
+// its own two C half tasks (row_done) and for nothing else: the warps that run this
+// function work beside the warps that still multiply. Rows come from a queue, longest
+// first. cos/sin(m alpha) follow the row by the angle recurrence of pipeline.cpp:70-79
+// from (1, 0), the operations that the reference uses to fill its table. Entered
+// through a pointer (g_rows_fn), once per warp and phase, so everything that does not
+// depend on the row stays in registers.
+// 256-bit (double) / 128-bit (float) gather of four consecutive values
+__device__ __forceinline__ void load4_cg(const double* p, double (&x)[4]) {
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void load4_cg(const float* p, float (&x)[4]) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+    x[0] = v.x;
+    x[1] = v.y;
+    x[2] = v.z;
+    x[3] = v.w;
+}
+
+// ROWS: the sources are in LAYOUT_ROWS (sfmm_internal.hpp): a lane reads re, im of two
+// consecutive m of its own source with one load and touches whole sectors only.
+template <int TL, bool ACC, bool ROWS>
+__device__ __noinline__ void elementwise_rows(const RowArgs e) {
     constexpr int L = 32 * TL;
+    constexpr int CHA = 2 * CHK;  // elements per batch of phase-A loads
     const int lane = threadIdx.x & 31;
-    Real* sm = reinterpret_cast<Real*>(smem_raw);
-    Real* buf = sm + e.buf_off + lane;
-    const Real* csd = sm + e.cs_d_off + lane;
-    const Real* csa = sm + e.cs_a_off + lane;
-    const int p_in = e.p_in, p_out = e.p_out, p_rot = e.p_rot;
-    const int p_max = max(p_in, p_out);
+    const int p_rot = e.p_rot;
+    const int i1 = min(1, p_rot - 1);  // row of cos/sin(alpha) in the tables
+    Real* buf = reinterpret_cast<Real*>(smem_raw) + e.buf_off + lane;
+    int* counters = reinterpret_cast<int*>(smem_raw + e.misc_off + 8);
+    const int* row_done = counters + 6;
     const bool do_d = e.geo_d != nullptr, do_a = e.geo_a != nullptr;
+    const GeoView<TL> gvd((do_d ? e.geo_d : e.geo_a) + lane, p_rot);
+    const GeoView<TL> gva((do_a ? e.geo_a : e.geo_d) + lane, p_rot);
 
-    auto rot_seek = [&](RotWalk<TL>& r, const TriWalk& w, const Real* ca, const Real* sa,
-                        const Real* qtab, const Real* basep) {
-        const int m = min(w.m, p_rot - 1), n = min(w.n, p_rot - 1);  // past the end: unused
-#pragma unroll
-        for (int t = 0; t < TL; ++t) {
-            r.c[t] = __ldcg(ca + m * L + 32 * t);
-            r.s[t] = __ldcg(sa + m * L + 32 * t);
-            r.qh[t] = __ldcg(qtab + m * L + 32 * t);
-            r.q[t] = __ldcg(qtab + n * L + 32 * t);
-            r.base[t] = __ldcg(basep + 32 * t);
-        }
-    };
-    auto rot_advance = [&](TriWalk& w, RotWalk<TL>& r, const Real* cs) {
-        ++w.n;
-#pragma unroll
-        for (int t = 0; t < TL; ++t) r.q[t] *= r.base[t];
-        if (w.n == w.p) {
-            ++w.m;
-            w.n = w.m;
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                const Real c1 = cs[32 * t], s1 = cs[L + 32 * t];
-                const Real nc = fma_(r.c[t], c1, -(r.s[t] * s1));
-                const Real ns = fma_(r.s[t], c1, r.c[t] * s1);
-                r.c[t] = nc;
-                r.s[t] = ns;
-                r.qh[t] *= r.base[t];
-                r.q[t] = r.qh[t];
-            }
-        }
-    };
-
-    TriWalk wd = tri_seek(CHK * e.c_lo, p_max), wa = wd;
-    RotWalk<TL> rd, ra;
-    int64_t bd[TL], srca[TL];
+    // per slot, for all rows. Idle slots of phase A (padding of the group, tail of the
+    // batch) need no masking of the data: their scale is 0 and, in accumulate mode, they
+    // read the source of the group's first pair, so a non-finite value can only reach a
+    // target that the reference poisons as well.
+    Real dc1[TL], ds1[TL], ac1[TL], as1[TL];
+    const Real* pa[TL];  // the slot's source: coefficient q at pa[t][q in_stride] (SoA), or
+                         // its expansion (ROWS)
+    int64_t bd[TL];
     bool actd[TL], acta[TL];
 #pragma unroll
     for (int t = 0; t < TL; ++t) {
+        dc1[t] = gvd.ca[i1 * L + 32 * t];
+        ds1[t] = gvd.sa[i1 * L + 32 * t];
+        ac1[t] = gva.ca[i1 * L + 32 * t];
+        as1[t] = gva.sa[i1 * L + 32 * t];
         bd[t] = e.g_d * L + 32 * t + lane;
-        actd[t] = do_d && bd[t] < e.n;
-        const int64_t bb = e.g_a * L + 32 * t + lane;
-        srca[t] = bb;
-        acta[t] = do_a && bb < e.n;
-        if (acta[t] && ACC) {
-            srca[t] = e.src_index[bb];
-            acta[t] = srca[t] >= 0;
+        actd[t] = bd[t] < e.n_total;
+        const int64_t g0 = e.g_a * L, bb = g0 + 32 * t + lane;
+        acta[t] = do_a && bb < e.n_total;
+        int64_t src = acta[t] ? bb : 0;
+        if (ACC && do_a) {
+            const int32_t s = e.src_index[acta[t] ? bb : g0];
+            acta[t] = acta[t] && s >= 0;
+            src = s >= 0 ? s : e.src_index[g0];
         }
-        if (!acta[t]) srca[t] = 0;
+        pa[t] = ROWS ? e.in + src * e.in_stride : e.in + src;
     }
-    if (do_d) {
-        const GeoView<TL> gv(e.geo_d + lane, p_rot);
-        rot_seek(rd, wd, gv.ca, gv.sa, gv.qd, gv.base_d);
-    }
-    if (do_a) {
-        const GeoView<TL> gv(e.geo_a + lane, p_rot);
-        rot_seek(ra, wa, gv.ca, gv.sa, gv.qa, gv.base_a);
-    }
+    const int p_max = max(e.p_in, e.p_out);
 
-    // ---- D on all chunks of the warp
-    if (do_d) {
-        for (int ci = e.c_lo; ci < e.c_hi; ++ci) {
-            if constexpr (!ACC) {
+    for (int task = fetch_task(&counters[3], lane); task < p_max;
+         task = fetch_task(&counters[3], lane)) {
+        const int n = p_max - 1 - task;
+        const bool row_d = do_d && n < e.p_out, row_a = do_a && n < e.p_in;
+        if (!row_d && !row_a) continue;
+        // row n of the triangle: re(m) at rowp[2 m L], im(m) at rowp[(2 m - 1) L]
+        Real* rowp = buf + n * n * L;
+
+        // ---- A, first part: the loads of the first batch are in flight during phase D
+        Real are[CHA][TL], aim[CHA][TL];
+        const int64_t row_off = ROWS ? rows_off(n) : (int64_t)aos_re(n, 0) * e.in_stride;
+        auto issue = [&](int m0) {
+            if constexpr (ROWS) {
 #pragma unroll
-                for (int u = 0; u < CHK; ++u) {
-                    if (wd.n < p_out) {
+                for (int j = 0; j < CHA / 2; ++j) {
+                    const int64_t off = row_off + 4 * min((m0 >> 1) + j, n >> 1);
 #pragma unroll
-                        for (int t = 0; t < TL; ++t) {
-                            const Real re = buf[t_re(wd.n, wd.m) * L + 32 * t];
-                            const Real im = wd.m ? buf[t_im(wd.n, wd.m) * L + 32 * t] : Real(0);
-                            const Real ms = -rd.s[t];
-                            const Real nr = rd.q[t] * fma_(re, rd.c[t], -(im * ms));
-                            const Real ni = rd.q[t] * fma_(re, ms, im * rd.c[t]);
-                            if (actd[t]) {
-                                const int64_t o = (int64_t)aos_re(wd.n, wd.m) * e.out_stride + bd[t];
-                                __stcg(e.out + o, nr);
-                                __stcg(e.out + o + e.out_stride, wd.m ? ni : Real(0));
-                            }
-                        }
+                    for (int t = 0; t < TL; ++t) {
+                        Real x[4];
+                        load4_cg(pa[t] + off, x);
+                        are[2 * j][t] = x[0];
+                        aim[2 * j][t] = x[1];
+                        are[2 * j + 1][t] = x[2];
+                        aim[2 * j + 1][t] = x[3];
                     }
-                    rot_advance(wd, rd, csd);
                 }
             } else {
+#pragma unroll
+                for (int u = 0; u < CHA; ++u) {
+                    const int64_t off = row_off + (int64_t)(2 * min(m0 + u, n)) * e.in_stride;
+#pragma unroll
+                    for (int t = 0; t < TL; ++t) {
+                        are[u][t] = __ldcg(pa[t] + off);
+                        aim[u][t] = __ldcg(pa[t] + off + e.in_stride);
+                    }
+                }
+            }
+        };
+        Real aq[TL];
+        if (row_a) {
+#pragma unroll
+            for (int t = 0; t < TL; ++t) aq[t] = acta[t] ? gva.qa[n * L + 32 * t] : Real(0);
+            issue(0);
+        }
+
+        // ---- D
+        if (row_d) {
+            Real c[TL], s[TL], q[TL];
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                q[t] = gvd.qd[n * L + 32 * t];
+                c[t] = Real(1);
+                s[t] = Real(0);
+            }
+            while (ld_volatile_shared(&row_done[n]) != 2 * e.gen) __nanosleep(32);
+            __threadfence_block();
+            for (int m0 = 0; m0 <= n; m0 += CHK) {
                 constexpr int NV = 2 * CHK, REP = 32 / NV;
                 Real v[NV];
-                int my_n = p_out, my_m = 0;  // the element whose sum this lane stores
+#pragma unroll
+                for (int j = 0; j < NV; ++j) v[j] = Real(0);
 #pragma unroll
                 for (int u = 0; u < CHK; ++u) {
+                    const int m = m0 + u;
+                    if (m > n) break;
                     Real sr = 0, si = 0;
-                    if (wd.n < p_out) {
 #pragma unroll
-                        for (int t = 0; t < TL; ++t) {
-                            const Real re = buf[t_re(wd.n, wd.m) * L + 32 * t];
-                            const Real im = wd.m ? buf[t_im(wd.n, wd.m) * L + 32 * t] : Real(0);
-                            const Real ms = -rd.s[t];
-                            const Real nr = rd.q[t] * fma_(re, rd.c[t], -(im * ms));
-                            const Real ni = rd.q[t] * fma_(re, ms, im * rd.c[t]);
+                    for (int t = 0; t < TL; ++t) {
+                        const Real re = rowp[(2 * m) * L + 32 * t];
+                        Real im = rowp[(2 * m - 1) * L + 32 * t];
+                        if (u == 0) im = m ? im : Real(0);  // column 0 has no imaginary part
+                        const Real ms = -s[t];
+                        const Real nr = q[t] * fma_(re, c[t], -(im * ms));
+                        const Real ni = q[t] * fma_(re, ms, im * c[t]);
+                        if constexpr (ACC) {
                             sr = t ? sr + nr : nr;
                             si = t ? si + ni : ni;
+                        } else {
+                            if (actd[t]) {
+                                const int64_t o = (int64_t)aos_re(n, m) * e.out_stride + bd[t];
+                                __stcg(e.out + o, nr);
+                                __stcg(e.out + o + e.out_stride, m ? ni : Real(0));
+                            }
                         }
+                        const Real nc = fma_(c[t], dc1[t], -(s[t] * ds1[t]));
+                        const Real ns = fma_(s[t], dc1[t], c[t] * ds1[t]);
+                        c[t] = nc;
+                        s[t] = ns;
                     }
                     v[2 * u] = sr;
                     v[2 * u + 1] = si;
-                    if (lane / (2 * REP) == u) {
-                        my_n = wd.n;
-                        my_m = wd.m;
-                    }
-                    rot_advance(wd, rd, csd);
                 }
-                lane_transpose_sum<NV>(v, lane);
-                // lanes REP k .. REP k + REP-1 hold value k: element k >> 1, part k & 1
-                const int part = (lane / REP) & 1;
-                if (!(lane & (REP - 1)) && my_n < p_out && !(part && my_m == 0))
-                    __stcg(e.out + (int64_t)(aos_re(my_n, my_m) + part) * e.out_stride + e.g_d, v[0]);
+                if constexpr (ACC) {
+                    lane_transpose_sum<NV>(v, lane);
+                    // lanes REP k .. REP k + REP-1 hold value k: element k >> 1, part k & 1
+                    const int k = lane / REP, m = m0 + (k >> 1), part = k & 1;
+                    if (!(lane & (REP - 1)) && m <= n && !(part && m == 0))
+                        __stcg(e.out + (int64_t)(aos_re(n, m) + part) * e.out_stride + e.g_d, v[0]);
+                }
             }
         }
-    }
-    if (!do_a) return;
+        if (!row_a) continue;
 
-    // ---- A on the same chunks, two chunks of loads in flight. The addresses are always
-    // valid (clamped; idle slots read source 0) and the values are zeroed only when
-    // consumed, so that neither a branch nor a use stands between the loads.
-    TriWalk wl = wa;  // load cursor, runs ahead of wa
-    auto issue = [&](Real (&re)[CHK][TL], Real (&im)[CHK][TL]) {
+        // ---- A, second part
+        Real c[TL], s[TL];
 #pragma unroll
-        for (int u = 0; u < CHK; ++u) {
-            const int64_t off =
-                (int64_t)aos_re(min(wl.n, p_in - 1), min(wl.m, p_in - 1)) * e.in_stride;
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                re[u][t] = __ldcg(e.in + off + srca[t]);
-                im[u][t] = __ldcg(e.in + off + e.in_stride + srca[t]);
-            }
-            wl.advance();
+        for (int t = 0; t < TL; ++t) {
+            c[t] = Real(1);
+            s[t] = Real(0);
         }
-    };
-    auto finish = [&](const Real (&re)[CHK][TL], const Real (&im)[CHK][TL]) {
+        for (int m0 = 0;;) {
 #pragma unroll
-        for (int u = 0; u < CHK; ++u) {
-            if (wa.n < p_in) {
+            for (int u = 0; u < CHA; ++u) {
+                const int m = m0 + u;
+                if (m > n) break;
 #pragma unroll
                 for (int t = 0; t < TL; ++t) {
-                    const Real xr = acta[t] ? re[u][t] : Real(0);
-                    const Real xi = (acta[t] && wa.m) ? im[u][t] : Real(0);
-                    const Real nr = ra.q[t] * fma_(xr, ra.c[t], -(xi * ra.s[t]));
-                    const Real ni = ra.q[t] * fma_(xr, ra.s[t], xi * ra.c[t]);
-                    buf[t_re(wa.n, wa.m) * L + 32 * t] = nr;
-                    if (wa.m) buf[t_im(wa.n, wa.m) * L + 32 * t] = ni;
+                    const Real xr = are[u][t];
+                    Real xi = aim[u][t];
+                    if (u == 0) xi = m ? xi : Real(0);
+                    const Real nr = aq[t] * fma_(xr, c[t], -(xi * s[t]));
+                    const Real ni = aq[t] * fma_(xr, s[t], xi * c[t]);
+                    rowp[(2 * m) * L + 32 * t] = nr;
+                    if (u || m) rowp[(2 * m - 1) * L + 32 * t] = ni;
+                    const Real nc = fma_(c[t], ac1[t], -(s[t] * as1[t]));
+                    const Real ns = fma_(s[t], ac1[t], c[t] * as1[t]);
+                    c[t] = nc;
+                    s[t] = ns;
                 }
             }
-            rot_advance(wa, ra, csa);
-        }
-    };
-    Real re0[CHK][TL], im0[CHK][TL], re1[CHK][TL], im1[CHK][TL];
-    if (e.c_lo < e.c_hi) issue(re0, im0);
-    for (int ci = e.c_lo; ci < e.c_hi; ci += 2) {
-        if (ci + 1 < e.c_hi) issue(re1, im1);
-        finish(re0, im0);
-        if (ci + 1 < e.c_hi) {
-            if (ci + 2 < e.c_hi) issue(re0, im0);
-            finish(re1, im1);
+            m0 += CHA;
+            if (m0 > n) break;
+            issue(m0);
         }
     }
 }
 
-// The elementwise phase is entered through a pointer read at run time: an indirect call
-// uses the plain calling convention, which gives the callee its own registers (a direct
-// call makes ptxas fit caller and callee into one register budget and starves it).
-using ElemFn = void (*)(const ElemArgs);
-__device__ ElemFn g_elem_fn[2] = {elementwise_phase<2, false>, elementwise_phase<2, true>};
+// The row loop is entered through a pointer read at run time: an indirect call uses the
+// plain calling convention, which gives the callee its own registers (with a direct call
+// ptxas fits caller and callee into one register budget and the callee spills the loads
+// it has in flight).
+using RowsFn = void (*)(const RowArgs);
+__device__ RowsFn g_rows_fn[4] = {elementwise_rows<2, false, false>, elementwise_rows<2, true, false>,
+                                  elementwise_rows<2, false, true>, elementwise_rows<2, true, true>};
 
 template <int TL>
 __global__ void __launch_bounds__(384, 1)
 translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, int p_rot,
                        int tab_len) {
-    constexpr int L = 32 * TL;
     if (a.fail_flag && *a.fail_flag) return;
 
     const int lane = threadIdx.x & 31;
@@ -803,9 +794,9 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
 
     Real* sm = reinterpret_cast<Real*>(smem_raw);
     Real* tab = sm;  // 16-byte aligned
-    Real* buf = sm + lay.tab_len + lane;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + lay.tab_len + lay.buf_elems());
-    int* counters = reinterpret_cast<int*>(mbar + 1);
+    int* counters = reinterpret_cast<int*>(mbar + 1);  // queues B, Z, C, rows; [4] finished C tasks
+    int* row_done = counters + 6;                      // [PMAX] finished C half tasks per row
     Real* geo_base = tt.scratch + (size_t)blockIdx.x * 2 * geo_elems<TL>(p_rot);
 
     const int kind = a.kind, p_in = a.p_in, p_out = a.p_out;
@@ -814,6 +805,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     const int side_fwd = src_local ? 1 : 0, side_bwd = dst_local ? 1 : 0;
     const bool two_sides = side_fwd != side_bwd;
     const int cols = min(p_in, p_out);
+    const int p_max = max(p_in, p_out);
     const bool accumulate = a.src_index != nullptr;
 
     // table staging: one mbarrier, completions alternate fwd / bwd tables
@@ -824,6 +816,8 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
                   mbar);
     }
     bool tab_pending = true;  // a bulk copy is in flight that the next swap phase must wait for
+    if (threadIdx.x < 6) counters[threadIdx.x] = 0;
+    if (threadIdx.x < PMAX) row_done[threadIdx.x] = 0;
 
     long long t_prev = clock64();
 #define SFMM_PHASE_MARK(idx)                                              \
@@ -832,56 +826,55 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         a.phase_clocks[idx] += now - t_prev;                              \
         t_prev = now;                                                     \
     }
-    // elementwise phases (elementwise_phase): warp w owns a contiguous run of chunks
-    const int p_max = max(p_in, p_out);
-    const int n_chunks = (p_max * (p_max + 1) / 2 + CHK - 1) / CHK;
-    const int cs_off = (int)(lay.tab_len + lay.buf_elems()) + 32 / (int)sizeof(Real);
-    Real* c1s1 = sm + cs_off;  // [2 groups][cos alpha | sin alpha][L]
-    ElemArgs ea;
-    ea.in = a.in;
-    ea.in_stride = a.in_stride;
-    ea.out = a.out;
-    ea.out_stride = a.out_stride;
-    ea.src_index = a.src_index;
-    ea.n = a.n;
-    ea.buf_off = (int)lay.tab_len;
-    ea.p_in = p_in;
-    ea.p_out = p_out;
-    ea.p_rot = p_rot;
-    ea.c_lo = n_chunks * warp / W;
-    ea.c_hi = n_chunks * (warp + 1) / W;
+    RowArgs ra;
+    ra.in = a.in;
+    ra.in_stride = a.in_stride;
+    ra.out = a.out;
+    ra.out_stride = a.out_stride;
+    ra.src_index = a.src_index;
+    ra.n_total = a.n;
+    ra.buf_off = (int)lay.tab_len;
+    ra.misc_off = (int)(sizeof(Real) * (lay.tab_len + lay.buf_elems()));
+    ra.p_in = p_in;
+    ra.p_out = p_out;
+    ra.p_rot = p_rot;
+    const RowsFn rows_fn = g_rows_fn[(accumulate ? 1 : 0) + (a.in_layout == LAYOUT_ROWS ? 2 : 0)];
+    // warps [0, n_cwarps) start the last phase with the C half tasks, the others with the rows
+    const int n_cwarps = W - max(1, W / 4);
 
-    // geometry and phase A of the first group; later groups are prepared one group
-    // ahead (geometry inside phase C, phase A fused behind phase D)
-    geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, c1s1, src_local, dst_local, warp, lane);
+    // geometry and phase A of the first group; later groups are prepared one group ahead
+    // (geometry during the z-step, phase A behind phase D of the same row)
+    geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, src_local, dst_local, warp, lane);
     __syncthreads();
-    ea.geo_d = nullptr;
-    ea.geo_a = geo_base;
-    ea.g_d = 0;
-    ea.g_a = blockIdx.x;
-    ea.cs_d_off = ea.cs_a_off = cs_off;
-    const ElemFn elem_fn = g_elem_fn[accumulate ? 1 : 0];
-    elem_fn(ea);
-    int parity = 0;
+    ra.geo_d = nullptr;
+    ra.geo_a = geo_base;
+    ra.g_d = 0;
+    ra.g_a = blockIdx.x;
+    ra.gen = 0;
+    rows_fn(ra);
+
+    // Schedule of one group (three CTA-wide barriers):
+    //   B    forward swap passes, one half task per (row, parity class);
+    //   Z    z-axis step per (column, re | im); the first TL warps first prepare the
+    //        geometry of the next group;
+    //   CDA  backward swap passes (C) on most warps; the other warps, and every warp
+    //        that finds the C queue empty, take rows from a second queue: phase D of
+    //        this group and phase A of the next one on a row whose two C half tasks are
+    //        done (row_done). The latency-bound elementwise work so runs beside the
+    //        multiplications instead of after them.
+    int parity = 0, gen = 0;
     for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x, parity ^= 1) {
         const GeoView<TL> gv(geo_base + (size_t)parity * geo_elems<TL>(p_rot) + lane, p_rot);
-        const GeoView<TL> gvn(geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot) + lane, p_rot);
         const bool has_next = g + gridDim.x < n_groups;
-        int64_t b[TL];
-        bool active[TL];
-#pragma unroll
-        for (int t = 0; t < TL; ++t) {
-            b[t] = g * L + 32 * t + lane;
-            active[t] = b[t] < a.n;
-        }
-        if (threadIdx.x == 0) counters[0] = counters[1] = counters[2] = 0;
+        ++gen;
         if (tab_pending) {
             mbar_wait(mbar, tab_phase);
             tab_phase ^= 1;
             tab_pending = false;
         }
-        __syncthreads();  // phase A of this group, its operator stream and the counters are in place
+        __syncthreads();  // phase A of this group and its operator stream are in place
         SFMM_PHASE_MARK(1)
+        if (threadIdx.x == 0) counters[2] = counters[3] = counters[4] = 0;
 
         // ---- B: forward swap passes, largest rows first
         {
@@ -894,12 +887,17 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         }
         __syncthreads();
         SFMM_PHASE_MARK(2)
+        if (threadIdx.x == 0) counters[0] = 0;
         if (two_sides) {  // stage the backward-side stream while the z-step runs
             if (threadIdx.x == 0) bulk_load(tab, tt.stream[side_bwd], tt.bytes[1], mbar);
             tab_pending = true;
         }
 
         // ---- Z: z-axis step per (column, re|im), longest columns first
+        if (has_next)
+            geometry_phase<TL>(a, g + gridDim.x, p_rot,
+                               geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot), src_local,
+                               dst_local, warp, lane);
         for (int task = fetch_task(&counters[1], lane); task < 2 * cols;
              task = fetch_task(&counters[1], lane)) {
             const int m = task >> 1, part = task & 1;
@@ -913,39 +911,35 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         }
         __syncthreads();
         SFMM_PHASE_MARK(3)
+        if (threadIdx.x == 0) counters[1] = 0;
 
-        // ---- C: backward swap passes; columns >= cols of the z-step output are
-        // zero (pipeline.cpp:229-246) and are skipped, which is exact. The first
-        // TL warps prepare the geometry of the NEXT group before joining the queue:
-        // its serial recurrences hide behind the other warps' products.
-        {
-            if (has_next)
-                geometry_phase<TL>(a, g + gridDim.x, p_rot,
-                                   geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot),
-                                   c1s1 + (parity ^ 1) * 2 * L, src_local, dst_local, warp, lane);
+        // ---- CDA. Columns >= cols of the z-step output are zero (pipeline.cpp:229-246)
+        // and are skipped by C, which is exact.
+        if (warp < n_cwarps) {
             Ctx<TL> c{(int)lay.tab_len, 0, gv.cb, gv.nsb, dst_local};
             for (int task = fetch_task(&counters[2], lane); task < 2 * p_out;
                  task = fetch_task(&counters[2], lane)) {
                 const int n = p_out - 1 - (task >> 1);
                 half_task_dispatch<TL>(c, n, task & 1, min(n, cols - 1));
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    atomicAdd(&row_done[n], 1);
+                    const int done = atomicAdd(&counters[4], 1) + 1;
+                    // the last C task frees the table: forward-side stream of the next group
+                    if (done == 2 * p_out && two_sides && has_next)
+                        bulk_load(tab, tt.stream[side_fwd], tt.bytes[0], mbar);
+                }
             }
         }
-        __syncthreads();
+        ra.geo_d = geo_base + (size_t)parity * geo_elems<TL>(p_rot);
+        ra.geo_a = has_next ? geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot) : nullptr;
+        ra.g_d = g;
+        ra.g_a = g + gridDim.x;
+        ra.gen = gen;
+        rows_fn(ra);
+        if (two_sides && has_next) tab_pending = true;
         SFMM_PHASE_MARK(4)
-        if (two_sides && has_next) {  // forward-side stream for the next group
-            if (threadIdx.x == 0) bulk_load(tab, tt.stream[side_fwd], tt.bytes[0], mbar);
-            tab_pending = true;
-        }
-
-        // ---- D of this group, A of the next one
-        ea.geo_d = geo_base + (size_t)parity * geo_elems<TL>(p_rot);
-        ea.geo_a = has_next ? geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot) : nullptr;
-        ea.g_d = g;
-        ea.g_a = g + gridDim.x;
-        ea.cs_d_off = cs_off + parity * 2 * L;
-        ea.cs_a_off = cs_off + (parity ^ 1) * 2 * L;
-        elem_fn(ea);
-        SFMM_PHASE_MARK(5)
     }
 #undef SFMM_PHASE_MARK
 }

@@ -355,7 +355,7 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
 
 template <typename Real>
 sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,
-                            const Real* d_src, int64_t src_stride, Real* d_out,
+                            const Real* d_src, int64_t src_stride, int src_layout, Real* d_out,
                             int64_t out_stride, cudaStream_t stream) {
     const int64_t so = solid_len(p_out);
     TranslateArgs<Real> a;
@@ -371,6 +371,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.n = plan->n_groups * kPlanGroup;
     a.in = d_src;
     a.in_stride = src_stride;
+    a.in_layout = src_layout;
     a.shifts = static_cast<const Real*>(plan->d_shifts);
     a.out = partial;
     a.out_stride = n_partial;
@@ -395,18 +396,18 @@ sfmm_status accumulate_host_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in
                                  const Real* src_aos, Real* out_aos) {
     const int64_t si = solid_len(p_in), so = solid_len(p_out);
     const int64_t ns = plan->n_sources, nt = plan->n_targets;
-    const int64_t sstride = round_up32(ns), ostride = round_up32(nt);
+    const int64_t srows = rows_off(p_in), ostride = round_up32(nt);
     cudaStream_t stream = nullptr;
     const size_t es = sizeof(Real);
     Real *d_src_aos = nullptr, *d_src = nullptr, *d_out = nullptr, *d_out_aos = nullptr;
     CU(cudaMallocAsync((void**)&d_src_aos, es * si * ns, stream));
-    CU(cudaMallocAsync((void**)&d_src, es * si * sstride, stream));
+    CU(cudaMallocAsync((void**)&d_src, es * srows * ns, stream));
     CU(cudaMallocAsync((void**)&d_out, es * so * ostride, stream));
     CU(cudaMallocAsync((void**)&d_out_aos, es * so * nt, stream));
     CU(cudaMemcpyAsync(d_src_aos, src_aos, es * si * ns, cudaMemcpyHostToDevice, stream));
-    CU(launch_pack_soa<Real>(d_src_aos, d_src, ns, p_in, sstride, stream));
-    sfmm_status st =
-        accumulate_impl<Real>(h, plan, p_in, p_out, d_src, sstride, d_out, ostride, stream);
+    CU(launch_pack_rows<Real>(d_src_aos, d_src, ns, p_in, stream));
+    sfmm_status st = accumulate_impl<Real>(h, plan, p_in, p_out, d_src, srows, LAYOUT_ROWS, d_out,
+                                           ostride, stream);
     if (st == SFMM_OK) {
         cudaError_t e = launch_unpack_soa<Real>(d_out, d_out_aos, nt, p_out, ostride, stream);
         if (e == cudaSuccess)
@@ -677,6 +678,22 @@ sfmm_status sfmm_pack_soa(sfmm_handle* h, int64_t n, int p, const void* d_aos, v
     return SFMM_OK;
 }
 
+int64_t sfmm_rows_len(int p) { return p < 1 ? 0 : rows_off(p); }
+
+sfmm_status sfmm_pack_rows(sfmm_handle* h, int64_t n, int p, const void* d_aos, void* d_rows,
+                           void* stream) {
+    if (!h || !d_aos || !d_rows || p < 1 || n < 0)
+        return fail(SFMM_INVALID_ARGUMENT, "bad pack_rows arguments");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    h->launches += 1;
+    if (h->precision == SFMM_F64)
+        CU(launch_pack_rows<double>((const double*)d_aos, (double*)d_rows, n, p, s));
+    else
+        CU(launch_pack_rows<float>((const float*)d_aos, (float*)d_rows, n, p, s));
+    return SFMM_OK;
+}
+
 sfmm_status sfmm_unpack_soa(sfmm_handle* h, int64_t n, int p, const void* d_soa, int64_t stride,
                             void* d_aos, void* stream) {
     if (!h || !d_aos || !d_soa || p < 1 || n < 0 || stride < n)
@@ -743,9 +760,30 @@ sfmm_status sfmm_m2l_accumulate(sfmm_handle* h, const sfmm_plan* plan, int p_in,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (h->precision == SFMM_F64)
         return accumulate_impl<double>(h, plan, p_in, p_out, (const double*)d_src, src_stride,
-                                       (double*)d_out, out_stride, s);
+                                       LAYOUT_SOA, (double*)d_out, out_stride, s);
     return accumulate_impl<float>(h, plan, p_in, p_out, (const float*)d_src, src_stride,
-                                  (float*)d_out, out_stride, s);
+                                  LAYOUT_SOA, (float*)d_out, out_stride, s);
+}
+
+sfmm_status sfmm_m2l_accumulate_rows(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,
+                                     const void* d_src_rows, void* d_out, int64_t out_stride,
+                                     void* stream) {
+    if (!h || !plan || plan->h != h) return fail(SFMM_INVALID_ARGUMENT, "plan/handle mismatch");
+    if (!d_src_rows || !d_out)
+        return fail(SFMM_INVALID_ARGUMENT, "translation request with null solid");
+    if (out_stride < plan->n_targets)
+        return fail(SFMM_INVALID_ARGUMENT, "batch stride smaller than the batch");
+    if (reinterpret_cast<uintptr_t>(d_src_rows) % 32)
+        return fail(SFMM_INVALID_ARGUMENT, "rows-layout sources must be 32-byte aligned");
+    const sfmm_status st = check_orders(h, SFMM_M2L, p_in, p_out);
+    if (st != SFMM_OK) return st;
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (h->precision == SFMM_F64)
+        return accumulate_impl<double>(h, plan, p_in, p_out, (const double*)d_src_rows,
+                                       rows_off(p_in), LAYOUT_ROWS, (double*)d_out, out_stride, s);
+    return accumulate_impl<float>(h, plan, p_in, p_out, (const float*)d_src_rows, rows_off(p_in),
+                                  LAYOUT_ROWS, (float*)d_out, out_stride, s);
 }
 
 sfmm_status sfmm_m2l_accumulate_host(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,

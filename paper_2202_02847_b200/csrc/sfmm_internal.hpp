@@ -11,6 +11,20 @@ namespace sfmm {
 
 enum : int { KIND_M2L = 0, KIND_M2M = 1, KIND_L2L = 2 };
 
+// Input layouts of a launch.
+//   LAYOUT_SOA   coefficient-major [c][stride]: unit-stride batches
+//   LAYOUT_ROWS  expansion-major [src][rows_len(p)]: the reference order (row n holds
+//                re, im of m = 0..n, solid.hpp:59-70) with every row padded to a multiple
+//                of four values, so that a lane that gathers its own source reads whole
+//                32-byte sectors (256-bit loads in double precision)
+enum : int { LAYOUT_SOA = 0, LAYOUT_ROWS = 1 };
+
+// first value of row n in LAYOUT_ROWS; rows_off(p) is the length of one expansion
+__host__ __device__ inline int rows_off(int n) {
+    const int a = n >> 1;
+    return 4 * (a + 1) * (a + (n & 1));
+}
+
 // Device-resident tables of one handle (precision Real).
 template <typename Real>
 struct DeviceTables {
@@ -31,8 +45,9 @@ struct TranslateArgs {
     int kind = 0;
     int p_in = 0, p_out = 0;
     int64_t n = 0;                // translations (lanes); in accumulate mode: padded pairs
-    const Real* in = nullptr;     // SoA [c][in_stride]
+    const Real* in = nullptr;     // SoA [c][in_stride], or rows [src][in_stride]
     int64_t in_stride = 0;
+    int in_layout = LAYOUT_SOA;
     const Real* shifts = nullptr; // [n][3]
     Real* out = nullptr;          // SoA [c][out_stride]; accumulate mode: partials [c][n/32]
     int64_t out_stride = 0;
@@ -82,6 +97,10 @@ cudaError_t launch_pack_soa(const Real* aos, Real* soa, int64_t n, int p, int64_
 template <typename Real>
 cudaError_t launch_unpack_soa(const Real* soa, Real* aos, int64_t n, int p, int64_t stride,
                               cudaStream_t stream);
+
+// AoS [n][P(P+1)] -> rows [n][rows_off(p)] (padding zeroed)
+template <typename Real>
+cudaError_t launch_pack_rows(const Real* aos, Real* rows, int64_t n, int p, cudaStream_t stream);
 
 // Accumulate mode, plan construction on the device (padding to groups + validation).
 template <typename Real>

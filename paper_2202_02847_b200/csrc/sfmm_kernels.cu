@@ -197,6 +197,29 @@ cudaError_t launch_unpack_soa(const Real* soa, Real* aos, int64_t n, int p, int6
     return cudaGetLastError();
 }
 
+// AoS -> rows: one thread per value of the padded layout.
+template <typename Real>
+__global__ void pack_rows_kernel(const Real* __restrict__ aos, Real* __restrict__ rows, int64_t n,
+                                 int p) {
+    const int R = rows_off(p), S = p * (p + 1);
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * R) return;
+    const int64_t b = i / R;
+    const int k = (int)(i - b * R);
+    int row = 0;
+    while (rows_off(row + 1) <= k) ++row;
+    const int j = k - rows_off(row);  // position in the row: 2 m + part
+    rows[i] = j < 2 * (row + 1) ? aos[b * S + row * (row + 1) + j] : Real(0);
+}
+
+template <typename Real>
+cudaError_t launch_pack_rows(const Real* aos, Real* rows, int64_t n, int p, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t total = n * rows_off(p);
+    pack_rows_kernel<Real><<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(aos, rows, n, p);
+    return cudaGetLastError();
+}
+
 template <typename Real>
 cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
                               const int32_t* grp_target, const int32_t* src_index,
@@ -281,6 +304,7 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
     template cudaError_t launch_check_shifts<Real>(const Real*, int64_t, int*, cudaStream_t);   \
     template cudaError_t launch_pack_soa<Real>(const Real*, Real*, int64_t, int, int64_t,       \
                                                cudaStream_t);                                   \
+    template cudaError_t launch_pack_rows<Real>(const Real*, Real*, int64_t, int, cudaStream_t); \
     template cudaError_t launch_unpack_soa<Real>(const Real*, Real*, int64_t, int, int64_t,     \
                                                  cudaStream_t);                                 \
     template cudaError_t launch_reduce_groups<Real>(const Real*, int64_t, const int64_t*, int,  \

@@ -220,6 +220,47 @@ def test_full_config3_level(oracle, h64):
     assert bits_equal(out2, 2.0 * out)                                          # scaling by 2 is exact
 
 
+def test_resident_accumulation_layouts(oracle, h64, h32):
+    """Device-pointer accumulation: SoA sources and rows-layout sources give the same bits
+    as the host call, with ragged targets (empty, one pair, > 64 pairs) in both precisions."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(97)
+    for h, p, dt, tdt in ((h64, 9, np.float64, torch.float64), (h32, 6, np.float32, torch.float32),
+                          (h64, 20, np.float64, torch.float64)):
+        ns = 45
+        counts = np.array([0, 1, 70, 3, 0, 64, 65, 130, 2])
+        tgt_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        idx = rng.integers(0, ns, int(tgt_ptr[-1])).astype(np.int32)
+        sh = random_shifts(rng, len(idx), with_axes=False).astype(dt)
+        src = random_solids(rng, ns, p).astype(dt)
+        plan = h.plan(tgt_ptr, idx, sh, ns)
+        want = plan.accumulate_host(p, p, src)
+        nt, S = len(counts), solid_size(p)
+        dev = torch.device("cuda", 0)
+        d_aos = torch.from_numpy(src).to(dev)
+        sstride, ostride = 64, 32
+        d_soa = torch.zeros((S, sstride), dtype=tdt, device=dev)
+        h.pack_soa(ns, p, d_aos.data_ptr(), d_soa.data_ptr(), sstride)
+        d_rows = torch.full((ns, h.rows_len(p)), float("nan"), dtype=tdt, device=dev)
+        h.pack_rows(ns, p, d_aos.data_ptr(), d_rows.data_ptr())
+        for mode in ("soa", "rows"):
+            d_out = torch.full((S, ostride), float("nan"), dtype=tdt, device=dev)
+            if mode == "soa":
+                plan.accumulate(p, p, d_soa.data_ptr(), sstride, d_out.data_ptr(), ostride)
+            else:
+                plan.accumulate_rows(p, p, d_rows.data_ptr(), d_out.data_ptr(), ostride)
+            torch.cuda.synchronize()
+            got = d_out.cpu().numpy()[:, :nt].T
+            # Im(C_n^0) is stored as zero by the reduction
+            assert bits_equal(got, want), (mode, p)
+        assert np.all(want[0] == 0) and np.all(want[4] == 0)                    # targets without pairs
+        if dt == np.float64:
+            _, per_pair = oracle.translate("m2l", p, p, src[idx], sh)
+            assert bits_equal(want, sharding.accumulation_tree(per_pair, tgt_ptr))
+        plan.close()
+    assert h64.rows_len(20) == 440 and h64.rows_len(1) == 4
+
+
 # ---- API contracts ---------------------------------------------------------
 
 def test_error_contracts(h64):

@@ -41,7 +41,13 @@ else:
     d_src = torch.empty((S, sstride), dtype=dt, device=dev)
     h.pack_soa(ns, P, d_aos.data_ptr(), d_src.data_ptr(), sstride, stream)
     d_out = torch.empty((S, ostride), dtype=dt, device=dev)
-    run = lambda: plan.accumulate(P, P, d_src.data_ptr(), sstride, d_out.data_ptr(), ostride, stream)
+    import os as _os
+    if _os.environ.get("SOA"):
+        run = lambda: plan.accumulate(P, P, d_src.data_ptr(), sstride, d_out.data_ptr(), ostride, stream)
+    else:
+        d_rows = torch.empty((ns, h.rows_len(P)), dtype=dt, device=dev)
+        h.pack_rows(ns, P, d_aos.data_ptr(), d_rows.data_ptr(), stream)
+        run = lambda: plan.accumulate_rows(P, P, d_rows.data_ptr(), d_out.data_ptr(), ostride, stream)
     units = int(tp[-1])
 
 import os
