@@ -220,18 +220,18 @@ def main():
     S = capi.solid_size(P)
     stream = torch.cuda.current_stream().cuda_stream
 
-    # ---- resident inputs (SoA) for the device-timed `value`
+    # ---- resident inputs for the device-timed `value`: sources in the library's rows
+    # layout (include/solidfmm_b200.h: sfmm_pack_rows), outputs SoA
     plan = handle.plan(my_ptr, my_idx, my_shifts, n_src)
-    sstride = (n_src + 31) // 32 * 32
     ostride = (my_targets + 31) // 32 * 32
     d_src_aos = torch.from_numpy(sources).to(dev)
-    d_src = torch.empty((S, sstride), dtype=torch.float64, device=dev)
-    handle.pack_soa(n_src, P, d_src_aos.data_ptr(), d_src.data_ptr(), sstride, stream)
+    d_src = torch.empty((n_src, handle.rows_len(P)), dtype=torch.float64, device=dev)
+    handle.pack_rows(n_src, P, d_src_aos.data_ptr(), d_src.data_ptr(), stream)
     d_out = torch.empty((S, ostride), dtype=torch.float64, device=dev)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step_resident():
-        plan.accumulate(P, P, d_src.data_ptr(), sstride, d_out.data_ptr(), ostride, stream)
+        plan.accumulate_rows(P, P, d_src.data_ptr(), d_out.data_ptr(), ostride, stream)
 
     def barrier():
         torch.cuda.synchronize()
@@ -265,12 +265,17 @@ def main():
 
     # ---- end to end through the host-buffer C-ABI call (plan from host arrays,
     # H2D of the sources, kernels, D2H of the local expansions), every step
-    out_host = np.empty((my_targets, S))
+    # host buffers are page-locked (the contract's "pinned host memory")
+    def pinned(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    h_ptr, h_idx, h_shifts, h_src = pinned(my_ptr), pinned(my_idx), pinned(my_shifts), pinned(sources)
+    out_host = torch.empty((my_targets, S), dtype=torch.float64).pin_memory().numpy()
     e2e_steps = max(2, min(args.steps, 5))
 
     def step_e2e():
-        p = handle.plan(my_ptr, my_idx, my_shifts, n_src)
-        p.accumulate_host(P, P, sources, out_host)
+        p = handle.plan(h_ptr, h_idx, h_shifts, n_src)
+        p.accumulate_host(P, P, h_src, out_host)
         p.close()
 
     step_e2e()
@@ -312,7 +317,7 @@ def main():
             "clocks": clocks,
             "e2e": {"value": total_pairs / worst_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "path": "sfmm_plan_create + sfmm_m2l_accumulate_host from pageable host arrays"},
+                    "path": "sfmm_plan_create + sfmm_m2l_accumulate_host from pinned host arrays"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak,

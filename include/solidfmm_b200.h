@@ -144,6 +144,9 @@ sfmm_status sfmm_plan_create(sfmm_handle* h, int64_t n_targets,
                              const int64_t* tgt_ptr, const int32_t* src_index,
                              const void* shifts, int64_t n_sources,
                              sfmm_plan** out);
+/* Frees the plan behind the work already enqueued on the default stream and on
+ * blocking streams; callers that launch on non-blocking streams synchronise
+ * them first. */
 void sfmm_plan_destroy(sfmm_plan* plan);
 int64_t sfmm_plan_pairs(const sfmm_plan* plan);
 

@@ -38,6 +38,9 @@ namespace {
 
 using Real = SFMM_REAL;
 constexpr int PMAX = SFMM_PMAX;
+#ifndef SFMM_MAXTHREADS
+#define SFMM_MAXTHREADS 384
+#endif
 constexpr int NCMAX = PMAX / 2 + (PMAX & 1);  // largest parity-class size, rows n < PMAX
 constexpr int TAB_PAD = 64;                    // finite slack behind the staged stream prefix
 constexpr int ZSEG = 2 * PMAX + 8;             // one z-table segment
@@ -427,6 +430,7 @@ struct TiledTables {
     const Real* stream[2];  // global parity-block streams: [0] multipole side, [1] local side
     uint32_t bytes[2];      // bytes staged for the forward / backward pass
     Real* scratch;          // global, per CTA and group parity: geometry of the group (geo_elems)
+    int row_warps;          // warps that start the last phase in the row queue
 };
 
 // Per-group geometry in the global scratch (L2 resident, written one group ahead,
@@ -782,7 +786,7 @@ __device__ RowsFn g_rows_fn[4] = {elementwise_rows<2, false, false>, elementwise
                                   elementwise_rows<2, false, true>, elementwise_rows<2, true, true>};
 
 template <int TL>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(SFMM_MAXTHREADS, 1)
 translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, int p_rot,
                        int tab_len) {
     if (a.fail_flag && *a.fail_flag) return;
@@ -840,7 +844,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     ra.p_rot = p_rot;
     const RowsFn rows_fn = g_rows_fn[(accumulate ? 1 : 0) + (a.in_layout == LAYOUT_ROWS ? 2 : 0)];
     // warps [0, n_cwarps) start the last phase with the C half tasks, the others with the rows
-    const int n_cwarps = W - max(1, W / 4);
+    const int n_cwarps = W - min(max(tt.row_warps, 0), W - 1);
 
     // geometry and phase A of the first group; later groups are prepared one group ahead
     // (geometry during the z-step, phase A behind phase D of the same row)
@@ -987,10 +991,15 @@ cudaError_t ensure_constants() {
     return cudaSuccess;
 }
 
+int tiled_row_warps_for(int warps) {
+    if (const char* env = getenv("SFMM_TILED_ROW_WARPS")) return atoi(env);
+    return std::max(1, warps / 4);
+}
+
 int tiled_warps_for(int p_rot) {
     if (const char* env = getenv("SFMM_TILED_WARPS")) {
         const int w = atoi(env);
-        if (w >= 2 && w <= 12) return w;
+        if (w >= 2 && w <= SFMM_MAXTHREADS / 32) return w;
     }
     if (p_rot >= 12) return 12;
     return 4;
@@ -1034,6 +1043,7 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     tt.stream[1] = t.stream[1];
     tt.bytes[0] = (uint32_t)(staged(a.p_in) * sizeof(Real));
     tt.bytes[1] = (uint32_t)(staged(a.p_out) * sizeof(Real));
+    tt.row_warps = tiled_row_warps_for(block / 32);
     e = cudaMallocAsync((void**)&tt.scratch, sizeof(Real) * (size_t)grid * 2 * geo_elems<TL>(p_rot), stream);
     if (e != cudaSuccess) return e;
     kern<<<grid, block, smem, stream>>>(a, tt, n_groups, p_rot, (int)tab_len);

@@ -310,9 +310,11 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
     // validation (source range, zero shifts) happen there
     cudaStream_t stream = nullptr;
     const size_t padded = (size_t)std::max<int64_t>(n_groups, 1) * kPlanGroup;
-    CU(cudaMalloc((void**)&plan->d_grp_ptr, sizeof(int64_t) * grp_ptr.size()));
-    CU(cudaMalloc((void**)&plan->d_src_index, sizeof(int32_t) * padded));
-    CU(cudaMalloc(&plan->d_shifts, sizeof(Real) * padded * 3));
+    // stream-ordered allocations from the device pool (kept warm by sfmm_create): a plan
+    // per call costs no cudaMalloc / cudaFree round trips
+    CU(cudaMallocAsync((void**)&plan->d_grp_ptr, sizeof(int64_t) * grp_ptr.size(), stream));
+    CU(cudaMallocAsync((void**)&plan->d_src_index, sizeof(int32_t) * padded, stream));
+    CU(cudaMallocAsync(&plan->d_shifts, sizeof(Real) * padded * 3, stream));
     int64_t* d_tgt = nullptr;
     int32_t *d_gt = nullptr, *d_idx = nullptr;
     Real* d_sh = nullptr;
@@ -738,9 +740,10 @@ void sfmm_plan_destroy(sfmm_plan* plan) {
     if (!plan) return;
     if (plan->h) {
         DeviceGuard guard(plan->h->device);
-        cudaFree(plan->d_grp_ptr);
-        cudaFree(plan->d_src_index);
-        cudaFree(plan->d_shifts);
+        // ordered on the legacy default stream: behind all work of blocking streams
+        cudaFreeAsync(plan->d_grp_ptr, nullptr);
+        cudaFreeAsync(plan->d_src_index, nullptr);
+        cudaFreeAsync(plan->d_shifts, nullptr);
     }
     delete plan;
 }
