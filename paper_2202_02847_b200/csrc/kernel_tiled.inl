@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "device_math.cuh"
@@ -247,63 +248,86 @@ __device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax
     // ---- second products: re[cF] = A_F[cF, cls] u_re,  im[cG] = A_G[cG, cls] u_im.
     // Output class index r (m' = class + 2r), rows r .. r+3 per trip; contracted index
     // k < nc (u[k] == 0 beyond).
-#pragma unroll 1
-    for (int r = 0; r < nc; r += 4) {
-        Real acc[4][TL];
+    // trips of four rows while more than two are left, then one trip of two
+    // (ROWS/2 128-bit loads per contracted index)
+    auto rows_of = [&](auto rows_tag, const Real* base, int ldb, const Real (&u)[NCE][TL],
+                       Real (&acc)[4][TL]) {
+        constexpr int RW = decltype(rows_tag)::value;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < RW; ++j)
 #pragma unroll
             for (int t = 0; t < TL; ++t) acc[j][t] = Real(0);
-        const Real* base = tF2 + r;
 #pragma unroll
         for (int k = 0; k < NCE; ++k) {
-            const Vec2 a0 = *reinterpret_cast<const Vec2*>(base + k * ld);
-            const Vec2 a1 = *reinterpret_cast<const Vec2*>(base + k * ld + 2);
+            const Vec2 a0 = *reinterpret_cast<const Vec2*>(base + k * ldb);
+            Vec2 a1 = a0;
+            if constexpr (RW == 4) a1 = *reinterpret_cast<const Vec2*>(base + k * ldb + 2);
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
-                acc[0][t] = fma_(a0.x, ure[k][t], acc[0][t]);
-                acc[1][t] = fma_(a0.y, ure[k][t], acc[1][t]);
-                acc[2][t] = fma_(a1.x, ure[k][t], acc[2][t]);
-                acc[3][t] = fma_(a1.y, ure[k][t], acc[3][t]);
+                acc[0][t] = fma_(a0.x, u[k][t], acc[0][t]);
+                acc[1][t] = fma_(a0.y, u[k][t], acc[1][t]);
+                if constexpr (RW == 4) {
+                    acc[2][t] = fma_(a1.x, u[k][t], acc[2][t]);
+                    acc[3][t] = fma_(a1.y, u[k][t], acc[3][t]);
+                }
             }
         }
-        if (c.local_side && r == 0 && cF == 0) {
+    };
+    using Four = std::integral_constant<int, 4>;
+    using Two = std::integral_constant<int, 2>;
+    {
+        int r = 0;
+        Real acc[4][TL];
+#pragma unroll 1
+        for (; r + 2 < nc; r += 4) {
+            rows_of(Four{}, tF2 + r, ld, ure, acc);
+            if (c.local_side && r == 0 && cF == 0) {
 #pragma unroll
-            for (int t = 0; t < TL; ++t) acc[0][t] *= Real(2);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (r + j < nc) {
-#pragma unroll
-                for (int t = 0; t < TL; ++t) re_io[4 * (r + j) * L + 32 * t] = acc[j][t];
+                for (int t = 0; t < TL; ++t) acc[0][t] *= Real(2);
             }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (r + j < nc) {
+#pragma unroll
+                    for (int t = 0; t < TL; ++t) re_io[4 * (r + j) * L + 32 * t] = acc[j][t];
+                }
+        }
+        if (r < nc) {
+            rows_of(Two{}, tF2 + r, ld, ure, acc);
+            if (c.local_side && r == 0 && cF == 0) {
+#pragma unroll
+                for (int t = 0; t < TL; ++t) acc[0][t] *= Real(2);
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                if (r + j < nc) {
+#pragma unroll
+                    for (int t = 0; t < TL; ++t) re_io[4 * (r + j) * L + 32 * t] = acc[j][t];
+                }
+        }
     }
-#pragma unroll 1
-    for (int r = 0; r < nG; r += 4) {
+    {
+        int r = 0;
         Real acc[4][TL];
+#pragma unroll 1
+        for (; r + 2 < nG; r += 4) {
+            rows_of(Four{}, tG2 + r, ldG2, uim, acc);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < 4; ++j)
+                if (r + j < nG && r + j >= g0) {
 #pragma unroll
-            for (int t = 0; t < TL; ++t) acc[j][t] = Real(0);
-        const Real* base = tG2 + r;
-#pragma unroll
-        for (int k = 0; k < NCE; ++k) {
-            const Vec2 a0 = *reinterpret_cast<const Vec2*>(base + k * ldG2);
-            const Vec2 a1 = *reinterpret_cast<const Vec2*>(base + k * ldG2 + 2);
-#pragma unroll
-            for (int t = 0; t < TL; ++t) {
-                acc[0][t] = fma_(a0.x, uim[k][t], acc[0][t]);
-                acc[1][t] = fma_(a0.y, uim[k][t], acc[1][t]);
-                acc[2][t] = fma_(a1.x, uim[k][t], acc[2][t]);
-                acc[3][t] = fma_(a1.y, uim[k][t], acc[3][t]);
-            }
+                    for (int t = 0; t < TL; ++t) im_io[4 * (r + j) * L + 32 * t] = acc[j][t];
+                }
         }
+        if (r < nG) {
+            rows_of(Two{}, tG2 + r, ldG2, uim, acc);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (r + j < nG && r + j >= g0) {
+            for (int j = 0; j < 2; ++j)
+                if (r + j < nG && r + j >= g0) {
 #pragma unroll
-                for (int t = 0; t < TL; ++t) im_io[4 * (r + j) * L + 32 * t] = acc[j][t];
-            }
+                    for (int t = 0; t < TL; ++t) im_io[4 * (r + j) * L + 32 * t] = acc[j][t];
+                }
+        }
     }
 }
 
