@@ -624,7 +624,7 @@ __device__ __forceinline__ void load4_cg(const float* p, float (&x)[4]) {
 template <int TL, bool ACC, bool ROWS>
 __device__ __noinline__ void elementwise_rows(const RowArgs e) {
     constexpr int L = 32 * TL;
-    constexpr int CHA = 2 * CHK;  // elements per batch of phase-A loads
+    constexpr int CHA = CHK;  // elements per batch of phase-A loads
     const int lane = threadIdx.x & 31;
     const int p_rot = e.p_rot;
     const int i1 = min(1, p_rot - 1);  // row of cos/sin(alpha) in the tables
