@@ -1017,7 +1017,8 @@ cudaError_t ensure_constants() {
 
 int tiled_row_warps_for(int warps) {
     if (const char* env = getenv("SFMM_TILED_ROW_WARPS")) return atoi(env);
-    return std::max(1, warps / 4);
+    // few warps (small orders): all warps finish the C queue first (measured)
+    return warps >= 8 ? warps / 4 : 0;
 }
 
 int tiled_warps_for(int p_rot) {
