@@ -323,11 +323,11 @@ def main():
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                          # dram__bytes_read.sum + dram__bytes_write.sum of translate_tiled_kernel,
                          # one ncu --set full capture of this workload at N=1
-                         # (profiles/ncu_full_translate_tiled_r01.csv): 125 MB read + 745 MB
+                         # (profiles/ncu_full_translate_tiled_r01.csv): 114 MB read + 460 MB
                          # written. Algorithmic: 65 MB sources + 82 MB partial sums + 43 MB
                          # pair list; the rest of the writes is L2 write-back of the register
                          # save area of the out-of-line row function (profiles/ncu_r01_notes.md)
-                         "traffic": 870.0e6 if world == 1 else None,
+                         "traffic": 573.5e6 if world == 1 else None,
                          "peak_source": "sfmm_measure_fma_peak (DFMA, measured in this run); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
                          "flops_per_translation": flops},
