@@ -254,6 +254,17 @@ def test_resident_accumulation_layouts(oracle, h64, h32):
             # Im(C_n^0) is stored as zero by the reduction
             assert bits_equal(got, want), (mode, p)
         assert np.all(want[0] == 0) and np.all(want[4] == 0)                    # targets without pairs
+        # the generic kernel reads the rows layout as well (32-lane groups: another tree)
+        h.set_option("kernel_variant", GENERIC)
+        try:
+            d_out = torch.full((S, ostride), float("nan"), dtype=tdt, device=dev)
+            plan.accumulate_rows(p, p, d_rows.data_ptr(), d_out.data_ptr(), ostride)
+            torch.cuda.synchronize()
+            tol = 1e-13 if dt == np.float64 else 2e-6
+            assert normalized_error(d_out.cpu().numpy()[:, :nt].T.astype(np.float64),
+                                    want.astype(np.float64)) < tol
+        finally:
+            h.set_option("kernel_variant", 0)
         if dt == np.float64:
             _, per_pair = oracle.translate("m2l", p, p, src[idx], sh)
             assert bits_equal(want, sharding.accumulation_tree(per_pair, tgt_ptr))
