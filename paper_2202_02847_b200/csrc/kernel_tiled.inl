@@ -498,15 +498,27 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
     if (warp >= TL) return;
     const int t = warp;
     const int64_t b = g * L + 32 * t + lane;
-    bool active = b < a.n;
-    if (active && a.src_index) active = a.src_index[b] >= 0;
-    Real x = 0, y = 0, z = 1;  // idle lanes get a benign shift (pipeline.cpp:56-61)
-    if (active) {
-        x = a.shifts[3 * b];
-        y = a.shifts[3 * b + 1];
-        z = a.shifts[3 * b + 2];
+    Angles<Real> ang;
+    Real inv;
+    if (a.angles) {  // plan path: decomposed when the plan was built, for every padded lane
+        ang.rn = a.angles[b];
+        ang.ca = a.angles[a.n + b];
+        ang.sa = a.angles[2 * a.n + b];
+        ang.cb = a.angles[3 * a.n + b];
+        ang.sb = a.angles[4 * a.n + b];
+        inv = a.angles[5 * a.n + b];
+    } else {
+        bool active = b < a.n;
+        if (active && a.src_index) active = a.src_index[b] >= 0;
+        Real x = 0, y = 0, z = 1;  // idle lanes get a benign shift (pipeline.cpp:56-61)
+        if (active) {
+            x = a.shifts[3 * b];
+            y = a.shifts[3 * b + 1];
+            z = a.shifts[3 * b + 2];
+        }
+        ang = decompose_angles(x, y, z);
+        inv = Real(1) / ang.rn;
     }
-    const Angles<Real> ang = decompose_angles(x, y, z);
     const GeoView<TL> v(geo + 32 * t + lane, p_rot);
     Real* cbg = const_cast<Real*>(v.cb);
     Real* sbg = const_cast<Real*>(v.sb);
@@ -515,7 +527,6 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
     Real* sag = const_cast<Real*>(v.sa);
     Real* qag = const_cast<Real*>(v.qa);
     Real* qdg = const_cast<Real*>(v.qd);
-    const Real inv = Real(1) / ang.rn;
     const Real base_a = src_local ? ang.rn : inv;
     const Real base_d = dst_local ? inv : ang.rn;
     *const_cast<Real*>(v.base_a) = base_a;

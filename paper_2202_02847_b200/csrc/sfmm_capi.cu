@@ -79,6 +79,7 @@ struct sfmm_plan {
     int64_t* d_grp_ptr = nullptr;   // [n_targets + 1]
     int32_t* d_src_index = nullptr; // [n_groups * 64], -1 = idle lane
     void* d_shifts = nullptr;       // [n_groups * 64][3]
+    void* d_angles = nullptr;       // [6][n_groups * 64]: decomposed shifts (TranslateArgs::angles)
 };
 
 namespace {
@@ -315,6 +316,7 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
     CU(cudaMallocAsync((void**)&plan->d_grp_ptr, sizeof(int64_t) * grp_ptr.size(), stream));
     CU(cudaMallocAsync((void**)&plan->d_src_index, sizeof(int32_t) * padded, stream));
     CU(cudaMallocAsync(&plan->d_shifts, sizeof(Real) * padded * 3, stream));
+    CU(cudaMallocAsync(&plan->d_angles, sizeof(Real) * padded * 6, stream));
     int64_t* d_tgt = nullptr;
     int32_t *d_gt = nullptr, *d_idx = nullptr;
     Real* d_sh = nullptr;
@@ -340,7 +342,7 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
     }
     CU(launch_build_plan<Real>(d_tgt, plan->d_grp_ptr, d_gt, d_idx, d_sh, n_groups, n_sources,
                                kPlanGroup, plan->d_src_index, static_cast<Real*>(plan->d_shifts),
-                               d_flags, stream));
+                               static_cast<Real*>(plan->d_angles), d_flags, stream));
     h->launches += 1;
     int flags[2] = {0, 0};
     CU(cudaMemcpyAsync(flags, d_flags, sizeof(flags), cudaMemcpyDeviceToHost, stream));
@@ -375,6 +377,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.in_stride = src_stride;
     a.in_layout = src_layout;
     a.shifts = static_cast<const Real*>(plan->d_shifts);
+    a.angles = static_cast<const Real*>(plan->d_angles);
     a.out = partial;
     a.out_stride = n_partial;
     a.src_index = plan->d_src_index;
@@ -744,6 +747,7 @@ void sfmm_plan_destroy(sfmm_plan* plan) {
         cudaFreeAsync(plan->d_grp_ptr, nullptr);
         cudaFreeAsync(plan->d_src_index, nullptr);
         cudaFreeAsync(plan->d_shifts, nullptr);
+        cudaFreeAsync(plan->d_angles, nullptr);
     }
     delete plan;
 }

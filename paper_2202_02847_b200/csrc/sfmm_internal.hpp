@@ -49,6 +49,9 @@ struct TranslateArgs {
     int64_t in_stride = 0;
     int in_layout = LAYOUT_SOA;
     const Real* shifts = nullptr; // [n][3]
+    // optional, plan path: the decomposed shifts [6][n] = |r|, cos/sin alpha, cos/sin beta,
+    // 1/|r| (geometry.cpp:11-30), computed once when the plan is built
+    const Real* angles = nullptr;
     Real* out = nullptr;          // SoA [c][out_stride]; accumulate mode: partials [c][n/32]
     int64_t out_stride = 0;
     const int32_t* src_index = nullptr;  // accumulate mode: source per lane, -1 = idle lane
@@ -107,7 +110,7 @@ template <typename Real>
 cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
                               const int32_t* grp_target, const int32_t* src_index,
                               const Real* shifts, int64_t n_groups, int64_t n_sources, int group,
-                              int32_t* out_index, Real* out_shifts, int* flags,
+                              int32_t* out_index, Real* out_shifts, Real* out_angles, int* flags,
                               cudaStream_t stream);
 
 // Accumulate mode, second stage: out[c][t] = sum_{g in groups of t} partial[c][g],

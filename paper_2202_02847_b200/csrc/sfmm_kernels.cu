@@ -61,7 +61,8 @@ __global__ void build_plan_kernel(const int64_t* __restrict__ tgt_ptr,
                                   const int32_t* __restrict__ src_index,
                                   const Real* __restrict__ shifts, int64_t n_groups,
                                   int64_t n_sources, int group, int32_t* __restrict__ out_index,
-                                  Real* __restrict__ out_shifts, int* flags) {
+                                  Real* __restrict__ out_shifts, Real* __restrict__ out_angles,
+                                  int* flags) {
     const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (d >= n_groups * group) return;
     const int64_t g = d / group;
@@ -84,6 +85,16 @@ __global__ void build_plan_kernel(const int64_t* __restrict__ tgt_ptr,
     out_shifts[3 * d] = x;
     out_shifts[3 * d + 1] = y;
     out_shifts[3 * d + 2] = z;
+    // the decomposition the translation kernel would do per group (idle lanes: the benign
+    // shift (0, 0, 1)), with the same device code
+    const Angles<Real> ang = decompose_angles(x, y, z);
+    const int64_t n = n_groups * group;
+    out_angles[d] = ang.rn;
+    out_angles[n + d] = ang.ca;
+    out_angles[2 * n + d] = ang.sa;
+    out_angles[3 * n + d] = ang.cb;
+    out_angles[4 * n + d] = ang.sb;
+    out_angles[5 * n + d] = Real(1) / ang.rn;
 }
 
 template <typename Real>
@@ -224,14 +235,14 @@ template <typename Real>
 cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
                               const int32_t* grp_target, const int32_t* src_index,
                               const Real* shifts, int64_t n_groups, int64_t n_sources, int group,
-                              int32_t* out_index, Real* out_shifts, int* flags,
+                              int32_t* out_index, Real* out_shifts, Real* out_angles, int* flags,
                               cudaStream_t stream) {
     if (n_groups <= 0) return cudaSuccess;
     const int block = 256;
     const int64_t grid = (n_groups * group + block - 1) / block;
     build_plan_kernel<Real><<<(unsigned)grid, block, 0, stream>>>(
         tgt_ptr, grp_ptr, grp_target, src_index, shifts, n_groups, n_sources, group, out_index,
-        out_shifts, flags);
+        out_shifts, out_angles, flags);
     return cudaGetLastError();
 }
 
@@ -312,7 +323,7 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
     template int translate_group_size<Real>(const TranslateArgs<Real>&);                        \
     template cudaError_t launch_build_plan<Real>(const int64_t*, const int64_t*, const int32_t*, \
                                                  const int32_t*, const Real*, int64_t, int64_t, \
-                                                 int, int32_t*, Real*, int*, cudaStream_t);     \
+                                                 int, int32_t*, Real*, Real*, int*, cudaStream_t);     \
     template cudaError_t launch_translate<Real>(const DeviceTables<Real>&,                      \
                                                 const TranslateArgs<Real>&, int, cudaStream_t,  \
                                                 LaunchInfo*);
