@@ -531,7 +531,15 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
     const Real base_d = dst_local ? inv : ang.rn;
     *const_cast<Real*>(v.base_a) = base_a;
     *const_cast<Real*>(v.base_d) = base_d;
-    Real c = 1, s = 0, ca = 1, sa = 0;
+    // cos/sin(m alpha): only the first step is tabulated, the elementwise phases follow
+    // the rows by the same recurrence (elementwise_rows)
+    cag[0] = Real(1);
+    sag[0] = Real(0);
+    if (p_rot > 1) {
+        cag[L] = fma_(Real(1), ang.ca, -(Real(0) * ang.sa));
+        sag[L] = fma_(Real(0), ang.ca, Real(1) * ang.sa);
+    }
+    Real c = 1, s = 0;
     Real qa = src_local ? Real(1) : base_a;  // base_a^(0 + q0)
     Real qd = dst_local ? Real(1) : base_d;
     for (int m = 0; m < p_rot + 2; ++m) {
@@ -539,8 +547,6 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
         sbg[m * L] = s;
         nsbg[m * L] = -s;
         if (m < p_rot) {
-            cag[m * L] = ca;
-            sag[m * L] = sa;
             qag[m * L] = qa;
             qdg[m * L] = qd;
         }
@@ -548,10 +554,6 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
         const Real ns = fma_(s, ang.cb, c * ang.sb);
         c = nc;
         s = ns;
-        const Real nca = fma_(ca, ang.ca, -(sa * ang.sa));
-        const Real nsa = fma_(sa, ang.ca, ca * ang.sa);
-        ca = nca;
-        sa = nsa;
         qa *= base_a;
         qd *= base_d;
     }
