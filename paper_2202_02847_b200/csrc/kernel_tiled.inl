@@ -443,10 +443,11 @@ struct TiledLayout {
     int p_rot;
     size_t tab_len;  // staged stream elements (prefix + TAB_PAD, multiple of 4)
     __host__ __device__ size_t buf_elems() const { return (size_t)p_rot * p_rot * L; }
-    // triangle, staged stream, {mbarrier, 4 task counters} (32 bytes), per-row completion
-    // counters of the backward swap pass
+    // triangle, staged stream, {mbarrier, task counters} (32 bytes), per-row completion
+    // counters of the backward swap pass, launch constants of the row function
     __host__ __device__ size_t smem_bytes() const {
-        return sizeof(Real) * (buf_elems() + tab_len) + 32 + sizeof(int) * ((PMAX + 3) / 4 * 4);
+        return sizeof(Real) * (buf_elems() + tab_len) + 32 + sizeof(int) * ((PMAX + 3) / 4 * 4) +
+               128;  // RowConst
     }
 };
 
@@ -587,22 +588,24 @@ __device__ __forceinline__ int ld_volatile_shared(const int* p) {
     return *reinterpret_cast<const volatile int*>(p);
 }
 
-// Arguments of elementwise_rows (one call per warp and phase).
-struct RowArgs {
+// Launch constants of elementwise_rows, written once per CTA into shared memory (behind
+// row_done): arguments that travel through the calling convention cost local-memory
+// stores and loads on every call.
+struct RowConst {
     const Real* in;            // sources: SoA (in_stride between coefficients) or rows
     int64_t in_stride;         //          (in_stride between expansions), see ROWS below
     Real* out;                 // outputs or per-group partial sums (SoA)
     int64_t out_stride;
     const int32_t* src_index;  // accumulate mode: source of every pair, else null
     int64_t n_total;           // translations of the launch
-    const Real* geo_d;         // geometry scratch of the group phase D finishes, or null
-    const Real* geo_a;         // geometry scratch of the group phase A loads, or null
-    int64_t g_d, g_a;          // their group numbers
+    const Real* geo_base;      // geometry scratch of this CTA: [2 parities][geo_elems]
+    int64_t geo_stride;        // geo_elems
     int buf_off;               // element offset of the triangle in smem_raw
-    int misc_off;              // byte offset of {mbarrier, counters, row_done} in smem_raw
     int p_in, p_out, p_rot;
-    int gen;                   // groups this CTA has started: row_done[n] == 2 gen when row n is ready
 };
+// per-call flags of elementwise_rows
+enum : int { ROWS_D = 1, ROWS_A = 2, ROWS_PARITY_D = 4, ROWS_PARITY_A = 8, ROWS_MISC_SHIFT = 4 };
+constexpr int ROW_DONE_BYTES = sizeof(int) * ((PMAX + 3) / 4 * 4);
 
 // Phases D and A, row by row (reference pipeline.cpp:251-257 and :148-154):
 //   D (group g):   rotate by -alpha, scale by the row factor, then store (ACC = false)
@@ -635,18 +638,22 @@ __device__ __forceinline__ void load4_cg(const float* p, float (&x)[4]) {
 // ROWS: the sources are in LAYOUT_ROWS (sfmm_internal.hpp): a lane reads re, im of two
 // consecutive m of its own source with one load and touches whole sectors only.
 template <int TL, bool ACC, bool ROWS>
-__device__ __noinline__ void elementwise_rows(const RowArgs e) {
+__device__ __noinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int gen, int flags) {
     constexpr int L = 32 * TL;
     constexpr int CHA = CHK;  // elements per batch of phase-A loads
     const int lane = threadIdx.x & 31;
+    const int misc_off = flags >> ROWS_MISC_SHIFT;  // bytes: {mbarrier, counters, row_done, RowConst}
+    int* counters = reinterpret_cast<int*>(smem_raw + misc_off + 8);
+    const int* row_done = counters + 6;
+    const RowConst& e = *reinterpret_cast<const RowConst*>(smem_raw + misc_off + 32 + ROW_DONE_BYTES);
     const int p_rot = e.p_rot;
     const int i1 = min(1, p_rot - 1);  // row of cos/sin(alpha) in the tables
     Real* buf = reinterpret_cast<Real*>(smem_raw) + e.buf_off + lane;
-    int* counters = reinterpret_cast<int*>(smem_raw + e.misc_off + 8);
-    const int* row_done = counters + 6;
-    const bool do_d = e.geo_d != nullptr, do_a = e.geo_a != nullptr;
-    const GeoView<TL> gvd((do_d ? e.geo_d : e.geo_a) + lane, p_rot);
-    const GeoView<TL> gva((do_a ? e.geo_a : e.geo_d) + lane, p_rot);
+    const bool do_d = flags & ROWS_D, do_a = flags & ROWS_A;
+    const Real* geo_d = e.geo_base + ((flags & ROWS_PARITY_D) ? e.geo_stride : 0);
+    const Real* geo_a = e.geo_base + ((flags & ROWS_PARITY_A) ? e.geo_stride : 0);
+    const GeoView<TL> gvd((do_d ? geo_d : geo_a) + lane, p_rot);
+    const GeoView<TL> gva((do_a ? geo_a : geo_d) + lane, p_rot);
 
     // per slot, for all rows. Idle slots of phase A (padding of the group, tail of the
     // batch) need no masking of the data: their scale is 0 and, in accumulate mode, they
@@ -663,9 +670,9 @@ __device__ __noinline__ void elementwise_rows(const RowArgs e) {
         ds1[t] = gvd.sa[i1 * L + 32 * t];
         ac1[t] = gva.ca[i1 * L + 32 * t];
         as1[t] = gva.sa[i1 * L + 32 * t];
-        bd[t] = e.g_d * L + 32 * t + lane;
+        bd[t] = g_d * L + 32 * t + lane;
         actd[t] = bd[t] < e.n_total;
-        const int64_t g0 = e.g_a * L, bb = g0 + 32 * t + lane;
+        const int64_t g0 = g_a * L, bb = g0 + 32 * t + lane;
         acta[t] = do_a && bb < e.n_total;
         int64_t src = acta[t] ? bb : 0;
         if (ACC && do_a) {
@@ -731,7 +738,7 @@ __device__ __noinline__ void elementwise_rows(const RowArgs e) {
                 c[t] = Real(1);
                 s[t] = Real(0);
             }
-            while (ld_volatile_shared(&row_done[n]) != 2 * e.gen) __nanosleep(32);
+            while (ld_volatile_shared(&row_done[n]) != 2 * gen) __nanosleep(32);
             __threadfence_block();
             for (int m0 = 0; m0 <= n; m0 += CHK) {
                 constexpr int NV = 2 * CHK, REP = 32 / NV;
@@ -774,7 +781,7 @@ __device__ __noinline__ void elementwise_rows(const RowArgs e) {
                     // lanes REP k .. REP k + REP-1 hold value k: element k >> 1, part k & 1
                     const int k = lane / REP, m = m0 + (k >> 1), part = k & 1;
                     if (!(lane & (REP - 1)) && m <= n && !(part && m == 0))
-                        __stcg(e.out + (int64_t)(aos_re(n, m) + part) * e.out_stride + e.g_d, v[0]);
+                        __stcg(e.out + (int64_t)(aos_re(n, m) + part) * e.out_stride + g_d, v[0]);
                 }
             }
         }
@@ -818,7 +825,7 @@ __device__ __noinline__ void elementwise_rows(const RowArgs e) {
 // plain calling convention, which gives the callee its own registers (with a direct call
 // ptxas fits caller and callee into one register budget and the callee spills the loads
 // it has in flight).
-using RowsFn = void (*)(const RowArgs);
+using RowsFn = void (*)(int64_t, int64_t, int, int);
 __device__ RowsFn g_rows_fn[4] = {elementwise_rows<2, false, false>, elementwise_rows<2, true, false>,
                                   elementwise_rows<2, false, true>, elementwise_rows<2, true, true>};
 
@@ -867,18 +874,24 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         a.phase_clocks[idx] += now - t_prev;                              \
         t_prev = now;                                                     \
     }
-    RowArgs ra;
-    ra.in = a.in;
-    ra.in_stride = a.in_stride;
-    ra.out = a.out;
-    ra.out_stride = a.out_stride;
-    ra.src_index = a.src_index;
-    ra.n_total = a.n;
-    ra.buf_off = (int)lay.tab_len;
-    ra.misc_off = (int)(sizeof(Real) * (lay.tab_len + lay.buf_elems()));
-    ra.p_in = p_in;
-    ra.p_out = p_out;
-    ra.p_rot = p_rot;
+    const int misc_off = (int)(sizeof(Real) * (lay.tab_len + lay.buf_elems()));
+    static_assert(sizeof(RowConst) <= 128, "RowConst area");
+    if (threadIdx.x == 0) {
+        RowConst& rc = *reinterpret_cast<RowConst*>(smem_raw + misc_off + 32 + ROW_DONE_BYTES);
+        rc.in = a.in;
+        rc.in_stride = a.in_stride;
+        rc.out = a.out;
+        rc.out_stride = a.out_stride;
+        rc.src_index = a.src_index;
+        rc.n_total = a.n;
+        rc.geo_base = geo_base;
+        rc.geo_stride = (int64_t)geo_elems<TL>(p_rot);
+        rc.buf_off = (int)lay.tab_len;
+        rc.p_in = p_in;
+        rc.p_out = p_out;
+        rc.p_rot = p_rot;
+    }
+    const int rows_misc = misc_off << ROWS_MISC_SHIFT;
     const RowsFn rows_fn = g_rows_fn[(accumulate ? 1 : 0) + (a.in_layout == LAYOUT_ROWS ? 2 : 0)];
     // warps [0, n_cwarps) start the last phase with the C half tasks, the others with the rows
     const int n_cwarps = W - min(max(tt.row_warps, 0), W - 1);
@@ -887,12 +900,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     // (geometry during the z-step, phase A behind phase D of the same row)
     geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, src_local, dst_local, warp, lane);
     __syncthreads();
-    ra.geo_d = nullptr;
-    ra.geo_a = geo_base;
-    ra.g_d = 0;
-    ra.g_a = blockIdx.x;
-    ra.gen = 0;
-    rows_fn(ra);
+    rows_fn(0, blockIdx.x, 0, rows_misc | ROWS_A);
 
     // Schedule of one group (three CTA-wide barriers):
     //   B    forward swap passes, one half task per (row, parity class);
@@ -973,12 +981,11 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
                 }
             }
         }
-        ra.geo_d = geo_base + (size_t)parity * geo_elems<TL>(p_rot);
-        ra.geo_a = has_next ? geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot) : nullptr;
-        ra.g_d = g;
-        ra.g_a = g + gridDim.x;
-        ra.gen = gen;
-        rows_fn(ra);
+        // a warp that comes from the C queue enters the row function (it costs a few
+        // thousand cycles to enter) only while rows are left
+        if (warp >= n_cwarps || ld_volatile_shared(&counters[3]) < p_max)
+            rows_fn(g, g + gridDim.x, gen,
+                    rows_misc | ROWS_D | (has_next ? ROWS_A : 0) | (parity ? ROWS_PARITY_D : ROWS_PARITY_A));
         if (two_sides && has_next) tab_pending = true;
         SFMM_PHASE_MARK(4)
     }
