@@ -32,6 +32,9 @@ NVCC_FLAGS = [
     "-Xcompiler", "-ffp-contract=off",
     "--expt-relaxed-constexpr",
 ]
+# tuning build: per-phase cycle counters in the tiled kernel (tools/perf_probe.py PHASES=1)
+if os.environ.get("SFMM_PHASE_CLOCKS"):
+    NVCC_FLAGS.append("-DSFMM_PHASE_CLOCKS")
 
 
 def nvcc_path() -> str:

@@ -867,6 +867,10 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     if (threadIdx.x < 6) counters[threadIdx.x] = 0;
     if (threadIdx.x < PMAX) row_done[threadIdx.x] = 0;
 
+    // per-phase cycle counters of CTA 0 (tuning aid, tools/perf_probe.py PHASES=1): compiled in
+    // only with -DSFMM_PHASE_CLOCKS, because the running time stamp costs every warp a
+    // local-memory round trip per phase
+#ifdef SFMM_PHASE_CLOCKS
     long long t_prev = clock64();
 #define SFMM_PHASE_MARK(idx)                                              \
     if (a.phase_clocks && blockIdx.x == 0 && threadIdx.x == 0) {          \
@@ -874,6 +878,9 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         a.phase_clocks[idx] += now - t_prev;                              \
         t_prev = now;                                                     \
     }
+#else
+#define SFMM_PHASE_MARK(idx)
+#endif
     const int misc_off = (int)(sizeof(Real) * (lay.tab_len + lay.buf_elems()));
     static_assert(sizeof(RowConst) <= 128, "RowConst area");
     if (threadIdx.x == 0) {

@@ -1,5 +1,6 @@
 """Kernel-only timing probe (device-resident SoA), for tuning and ncu captures.
-usage: perf_probe.py [batched|level] [P] [n_or_grid] [reps]"""
+usage: perf_probe.py [batched|level] [P] [n_or_grid] [reps]
+PHASES=1 prints the per-phase cycle split of CTA 0 (library built with SFMM_PHASE_CLOCKS=1)."""
 import sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
