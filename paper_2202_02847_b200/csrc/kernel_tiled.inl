@@ -433,7 +433,10 @@ __device__ __forceinline__ void zstep_dispatch(int buf, int kind, int p_in, int 
 
 __device__ __forceinline__ int fetch_task(int* counter, int lane) {
     int t = 0;
-    if (lane == 0) t = atomicAdd(counter, 1);
+    // plain PTX: atomicAdd() under a lane predicate compiles to the warp-aggregated
+    // sequence (vote, find-leader, popc), a dozen instructions per fetch for nothing
+    if (lane == 0)
+        asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(t) : "r"(smem_u32(counter)) : "memory");
     return __shfl_sync(0xffffffffu, t, 0);
 }
 
