@@ -272,6 +272,32 @@ def test_resident_accumulation_layouts(oracle, h64, h32):
     assert h64.rows_len(20) == 440 and h64.rows_len(1) == 4
 
 
+def test_accumulation_mixed_orders(oracle, h64):
+    """Target-owned accumulation with p_in != p_out (rows that only phase A or only phases
+    C/D touch), both kernels, against the per-pair oracle results summed in the library's
+    documented order."""
+    rng = np.random.default_rng(101)
+    ns = 30
+    counts = np.array([3, 0, 67, 64, 1])
+    tgt_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    idx = rng.integers(0, ns, int(tgt_ptr[-1])).astype(np.int32)
+    sh = random_shifts(rng, len(idx), with_axes=False)
+    for p_in, p_out in ((12, 7), (7, 12), (20, 3), (1, 20), (5, 5)):
+        src = random_solids(rng, ns, p_in)
+        plan = h64.plan(tgt_ptr, idx, sh, ns)
+        _, per_pair = oracle.translate("m2l", p_in, p_out, src[idx], sh)
+        want = sharding.accumulation_tree(per_pair, tgt_ptr)
+        got = plan.accumulate_host(p_in, p_out, src)
+        assert bits_equal(got, want), (p_in, p_out)
+        h64.set_option("kernel_variant", GENERIC)
+        try:
+            got_g = plan.accumulate_host(p_in, p_out, src)
+        finally:
+            h64.set_option("kernel_variant", 0)
+        assert normalized_error(got_g, want) < 1e-13, (p_in, p_out)
+        plan.close()
+
+
 # ---- API contracts ---------------------------------------------------------
 
 def test_error_contracts(h64):
