@@ -297,6 +297,100 @@ float time_ms(F launch, int reps = 3) {
     return best;
 }
 
+
+// ---- 8. swap-product candidates with operands AND results in shared memory (what a half
+// task really does): Y[i][t] = sum_k A[i][k] X[k][t], NC x NC block, 64 translations per
+// warp-task, X rows in shared memory, Y stored back.
+//  (a) the shipped scheme: lane = 2 translations, entries by warp-uniform LDS.128;
+//  (b) DMMA m8n8k4: M = rows i, N = 8 translations, K = 4 inputs; A fragments from a
+//      fragment-major table (one conflict-free LDS.64 per lane), B fragments from X with an
+//      XOR swizzle of the translation index by the row so that the four rows of a fragment
+//      fall into different banks.
+template <int NC>
+__global__ void k_prod_dfma(double* out, int iters, const double* __restrict__ gtab) {
+    extern __shared__ __align__(16) double sm[];
+    constexpr int LD = NC + (NC & 1);
+    double* tab = sm;                                   // [NC][LD] lines
+    double* X = sm + 1024 + (threadIdx.x >> 5) * (16 * 64);  // per warp [16 rows][64]
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) tab[i] = gtab[i];
+    const int lane = threadIdx.x & 31;
+    for (int k = 0; k < 16; ++k) X[k * 64 + lane] = 0.001 * lane + k, X[k * 64 + 32 + lane] = 0.002 * lane - k;
+    __syncthreads();
+    for (int it = 0; it < iters; ++it) {
+        double acc[LD][2];
+#pragma unroll
+        for (int i = 0; i < LD; ++i) acc[i][0] = acc[i][1] = 0;
+#pragma unroll 2
+        for (int k = 0; k < NC; ++k) {
+            const double x0 = X[k * 64 + lane], x1 = X[k * 64 + 32 + lane];
+#pragma unroll
+            for (int i2 = 0; i2 < LD / 2; ++i2) {
+                const double2 a = *reinterpret_cast<const double2*>(tab + k * LD + 2 * i2);
+                acc[2 * i2][0] = fma(a.x, x0, acc[2 * i2][0]);
+                acc[2 * i2][1] = fma(a.x, x1, acc[2 * i2][1]);
+                acc[2 * i2 + 1][0] = fma(a.y, x0, acc[2 * i2 + 1][0]);
+                acc[2 * i2 + 1][1] = fma(a.y, x1, acc[2 * i2 + 1][1]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+            X[i * 64 + lane] = acc[i][0] * 1e-3;
+            X[i * 64 + 32 + lane] = acc[i][1] * 1e-3;
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = X[lane];
+}
+
+template <int NC>
+__global__ void k_prod_dmma(double* out, int iters, const double* __restrict__ gtab) {
+    extern __shared__ __align__(16) double sm[];
+    constexpr int MT = (NC + 7) / 8, KT = (NC + 3) / 4;
+    double* tab = sm;                                   // [KT][MT][32] fragment-major
+    double* X = sm + 1024 + (threadIdx.x >> 5) * (16 * 64);  // per warp [16 rows][64], swizzled
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) tab[i] = gtab[i];
+    const int lane = threadIdx.x & 31;
+    for (int k = 0; k < 16; ++k) X[k * 64 + lane] = 0.001 * lane + k, X[k * 64 + 32 + lane] = 0.002 * lane - k;
+    __syncthreads();
+    const int fk = lane & 3, fn = lane >> 2;  // B fragment: row k, column n; D: row fn, columns 2 fk, 2 fk + 1
+    for (int it = 0; it < iters; ++it) {
+        double d[MT][8][2];
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int n = 0; n < 8; ++n) d[m][n][0] = d[m][n][1] = 0;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+            double a[MT];
+#pragma unroll
+            for (int m = 0; m < MT; ++m) a[m] = tab[(kt * MT + m) * 32 + lane];
+            const int row = kt * 4 + fk;
+            const double* xr = X + row * 64;
+            const int swz = (row & 3) * 8;
+#pragma unroll
+            for (int n = 0; n < 8; ++n) {
+                const double b = xr[(n * 8 + fn) ^ swz];
+#pragma unroll
+                for (int m = 0; m < MT; ++m) dmma884(d[m][n][0], d[m][n][1], a[m], b);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            const int row = m * 8 + fn;
+            if (row < NC) {
+                const int swz = (row & 3) * 8;
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    double2 v;
+                    v.x = d[m][n][0] * 1e-3;
+                    v.y = d[m][n][1] * 1e-3;
+                    *reinterpret_cast<double2*>(X + row * 64 + ((n * 8 + 2 * fk) ^ swz)) = v;
+                }
+            }
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = X[lane];
+}
+
 int main(int argc, char** argv) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, 0));
@@ -429,6 +523,26 @@ int main(int argc, char** argv) {
             for (int i = 0; i < 64; ++i) mism += memcmp(&D[i], &R[i], 8) != 0;
         }
         printf("{\"test\": \"dmma_vs_fma_chain\", \"elements\": %d, \"mismatches\": %d}\n", trials * 64, mism);
+    }
+
+    {
+        auto run_prod = [&](auto kern, const char* name, int NC, int warps) {
+            const int block = warps * 32, grid = sms, iters = 20000;
+            const size_t smem = sizeof(double) * (1024 + warps * 16 * 64);
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            float ms = time_ms([&] { kern<<<grid, block, smem>>>(out, iters, gtab); });
+            double fl = 2.0 * NC * NC * 64 * (double)iters * grid * warps;
+            printf("{\"test\": \"%s\", \"NC\": %d, \"warps_per_sm\": %d, \"ms\": %.3f, \"useful_tflops\": %.2f}\n",
+                   name, NC, warps, ms, fl / ms * 1e-9);
+        };
+        for (int warps : {8, 12, 16}) {
+            run_prod(k_prod_dfma<10>, "prod_dfma_smem", 10, warps);
+            run_prod(k_prod_dmma<10>, "prod_dmma_smem", 10, warps);
+            run_prod(k_prod_dfma<8>, "prod_dfma_smem", 8, warps);
+            run_prod(k_prod_dmma<8>, "prod_dmma_smem", 8, warps);
+            run_prod(k_prod_dfma<6>, "prod_dfma_smem", 6, warps);
+            run_prod(k_prod_dmma<6>, "prod_dmma_smem", 6, warps);
+        }
     }
     return 0;
 }
