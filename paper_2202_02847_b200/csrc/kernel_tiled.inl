@@ -170,7 +170,7 @@ __device__ __forceinline__ void first_product(const Real* tab, int ld, const Rea
 // about 32 KB per SM and execution slows ~5x once the code the warps of an SM
 // run concurrently exceeds it (profiles/icache_probe_r01.jsonl). The warps of
 // a CTA work on different rows at the same time, so the half task exists in
-// only four sizes NCE in {4, 6, 8, 10} (~20 KB together), each out of line and
+// only five sizes NCE in {2, 4, 6, 8, 10}, each out of line and
 // shared by the forward and the backward pass; a class of nc = NCE-1 members
 // runs in the NCE code with one idle accumulator (the table lines are padded
 // to even length with zeros, so the idle lane stays exactly zero).
@@ -334,7 +334,8 @@ __device__ __noinline__ void half_task(const Ctx<TL> c, int n, int cls, int mmax
 template <int TL>
 __device__ __forceinline__ void half_task_dispatch(const Ctx<TL> c, int n, int cls, int mmax) {
     const int nc = class_size(n, cls);
-    if (nc <= 4) half_task<TL, 4>(c, n, cls, mmax);
+    if (nc <= 2) half_task<TL, 2>(c, n, cls, mmax);
+    else if (nc <= 4) half_task<TL, 4>(c, n, cls, mmax);
     else if (nc <= 6) half_task<TL, 6>(c, n, cls, mmax);
     else if (nc <= 8) {
         if constexpr (NCMAX > 6) half_task<TL, 8>(c, n, cls, mmax);
