@@ -642,7 +642,7 @@ __device__ __forceinline__ void load4_cg(const float* p, float (&x)[4]) {
 // ROWS: the sources are in LAYOUT_ROWS (sfmm_internal.hpp): a lane reads re, im of two
 // consecutive m of its own source with one load and touches whole sectors only.
 template <int TL, bool ACC, bool ROWS>
-__device__ __noinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int gen, int flags) {
+__device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int gen, int flags) {
     constexpr int L = 32 * TL;
     constexpr int CHA = CHK;  // elements per batch of phase-A loads
     const int lane = threadIdx.x & 31;
@@ -825,15 +825,7 @@ __device__ __noinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int gen,
     }
 }
 
-// The row loop is entered through a pointer read at run time: an indirect call uses the
-// plain calling convention, which gives the callee its own registers (with a direct call
-// ptxas fits caller and callee into one register budget and the callee spills the loads
-// it has in flight).
-using RowsFn = void (*)(int64_t, int64_t, int, int);
-__device__ RowsFn g_rows_fn[4] = {elementwise_rows<2, false, false>, elementwise_rows<2, true, false>,
-                                  elementwise_rows<2, false, true>, elementwise_rows<2, true, true>};
-
-template <int TL>
+template <int TL, bool ACC, bool ROWS>
 __global__ void __launch_bounds__(SFMM_MAXTHREADS, 1)
 translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, int p_rot,
                        int tab_len) {
@@ -903,36 +895,68 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         rc.p_rot = p_rot;
     }
     const int rows_misc = misc_off << ROWS_MISC_SHIFT;
-    const RowsFn rows_fn = g_rows_fn[(accumulate ? 1 : 0) + (a.in_layout == LAYOUT_ROWS ? 2 : 0)];
     // warps [0, n_cwarps) start the last phase with the C half tasks, the others with the rows
     const int n_cwarps = W - min(max(tt.row_warps, 0), W - 1);
 
-    // geometry and phase A of the first group; later groups are prepared one group ahead
-    // (geometry during the z-step, phase A behind phase D of the same row)
+    // geometry of the first group; later groups are prepared one group ahead (geometry during
+    // the z-step, phase A behind phase D of the same row)
     geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, src_local, dst_local, warp, lane);
     __syncthreads();
-    rows_fn(0, blockIdx.x, 0, rows_misc | ROWS_A);
 
-    // Schedule of one group (three CTA-wide barriers):
-    //   B    forward swap passes, one half task per (row, parity class);
-    //   Z    z-axis step per (column, re | im); the first TL warps first prepare the
-    //        geometry of the next group;
-    //   CDA  backward swap passes (C) on most warps; the other warps, and every warp
-    //        that finds the C queue empty, take rows from a second queue: phase D of
-    //        this group and phase A of the next one on a row whose two C half tasks are
-    //        done (row_done). The latency-bound elementwise work so runs beside the
-    //        multiplications instead of after them.
-    int parity = 0, gen = 0;
-    for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x, parity ^= 1) {
+    // Schedule (three CTA-wide barriers per group). One trip of the loop:
+    //   CDA  of the group `cur` that has finished its z-step (none in the first trip):
+    //        backward swap passes (C) on most warps; the other warps, and every warp that
+    //        finds the C queue empty, take rows from a second queue: phase D of `cur` and
+    //        phase A of `nxt` on a row whose two C half tasks are done (row_done). The
+    //        latency-bound elementwise work so runs beside the multiplications;
+    //   B    of `nxt`: forward swap passes, one half task per (row, parity class);
+    //   Z    of `nxt`: z-axis step per (column, re | im); the first TL warps first prepare
+    //        the geometry of the group after it.
+    // The row code is inline at this one place (out of line, called directly, ptxas fits
+    // caller and callee into one register budget and spills the loads in flight).
+    int parity = 0, gen = 0;  // parity: geometry buffer of `nxt`
+    int64_t cur = -1;
+    for (int64_t nxt = blockIdx.x;; nxt += gridDim.x, parity ^= 1) {
+        const bool has_next = nxt < n_groups;
+        if (cur >= 0 && warp < n_cwarps) {
+            // ---- C of `cur`. Columns >= cols of the z-step output are zero
+            // (pipeline.cpp:229-246) and are skipped, which is exact.
+            const GeoView<TL> gv(geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot) + lane, p_rot);
+            Ctx<TL> c{(int)lay.tab_len, 0, gv.cb, gv.nsb, dst_local};
+            for (int task = fetch_task(&counters[2], lane); task < 2 * p_out;
+                 task = fetch_task(&counters[2], lane)) {
+                const int n = p_out - 1 - (task >> 1);
+                half_task_dispatch<TL>(c, n, task & 1, min(n, cols - 1));
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    atomicAdd(&row_done[n], 1);
+                    const int done = atomicAdd(&counters[4], 1) + 1;
+                    // the last C task frees the table: forward-side stream of the next group
+                    if (done == 2 * p_out && two_sides && has_next)
+                        bulk_load(tab, tt.stream[side_fwd], tt.bytes[0], mbar);
+                }
+            }
+        }
+        // ---- D of `cur`, A of `nxt`
+        if (cur >= 0 || has_next)
+            elementwise_rows<TL, ACC, ROWS>(
+                cur, nxt, gen,
+                rows_misc | (cur >= 0 ? ROWS_D : 0) | (has_next ? ROWS_A : 0) |
+                    (parity ? ROWS_PARITY_A : ROWS_PARITY_D));
+        if (!has_next) break;
+        if (cur >= 0 && two_sides) tab_pending = true;
+        SFMM_PHASE_MARK(4)
+
         const GeoView<TL> gv(geo_base + (size_t)parity * geo_elems<TL>(p_rot) + lane, p_rot);
-        const bool has_next = g + gridDim.x < n_groups;
+        const bool more = nxt + gridDim.x < n_groups;
         ++gen;
         if (tab_pending) {
             mbar_wait(mbar, tab_phase);
             tab_phase ^= 1;
             tab_pending = false;
         }
-        __syncthreads();  // phase A of this group and its operator stream are in place
+        __syncthreads();  // phase A of `nxt` and its operator stream are in place
         SFMM_PHASE_MARK(1)
         if (threadIdx.x == 0) counters[2] = counters[3] = counters[4] = 0;
 
@@ -954,8 +978,8 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         }
 
         // ---- Z: z-axis step per (column, re|im), longest columns first
-        if (has_next)
-            geometry_phase<TL>(a, g + gridDim.x, p_rot,
+        if (more)
+            geometry_phase<TL>(a, nxt + gridDim.x, p_rot,
                                geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot), src_local,
                                dst_local, warp, lane);
         for (int task = fetch_task(&counters[1], lane); task < 2 * cols;
@@ -972,33 +996,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         __syncthreads();
         SFMM_PHASE_MARK(3)
         if (threadIdx.x == 0) counters[1] = 0;
-
-        // ---- CDA. Columns >= cols of the z-step output are zero (pipeline.cpp:229-246)
-        // and are skipped by C, which is exact.
-        if (warp < n_cwarps) {
-            Ctx<TL> c{(int)lay.tab_len, 0, gv.cb, gv.nsb, dst_local};
-            for (int task = fetch_task(&counters[2], lane); task < 2 * p_out;
-                 task = fetch_task(&counters[2], lane)) {
-                const int n = p_out - 1 - (task >> 1);
-                half_task_dispatch<TL>(c, n, task & 1, min(n, cols - 1));
-                __syncwarp();
-                if (lane == 0) {
-                    __threadfence_block();
-                    atomicAdd(&row_done[n], 1);
-                    const int done = atomicAdd(&counters[4], 1) + 1;
-                    // the last C task frees the table: forward-side stream of the next group
-                    if (done == 2 * p_out && two_sides && has_next)
-                        bulk_load(tab, tt.stream[side_fwd], tt.bytes[0], mbar);
-                }
-            }
-        }
-        // a warp that comes from the C queue enters the row function (it costs a few
-        // thousand cycles to enter) only while rows are left
-        if (warp >= n_cwarps || ld_volatile_shared(&counters[3]) < p_max)
-            rows_fn(g, g + gridDim.x, gen,
-                    rows_misc | ROWS_D | (has_next ? ROWS_A : 0) | (parity ? ROWS_PARITY_D : ROWS_PARITY_A));
-        if (two_sides && has_next) tab_pending = true;
-        SFMM_PHASE_MARK(4)
+        cur = nxt;
     }
 #undef SFMM_PHASE_MARK
 }
@@ -1085,7 +1083,9 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     const size_t smem = lay.smem_bytes();
     const int64_t n_groups = (a.n + L - 1) / L;
     const int block = 32 * tiled_warps_for(p_rot);
-    auto kern = translate_tiled_kernel<TL>;
+    const bool acc = a.src_index != nullptr, rows = a.in_layout == LAYOUT_ROWS;
+    auto kern = acc ? (rows ? translate_tiled_kernel<TL, true, true> : translate_tiled_kernel<TL, true, false>)
+                    : (rows ? translate_tiled_kernel<TL, false, true> : translate_tiled_kernel<TL, false, false>);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
