@@ -644,7 +644,7 @@ __device__ __forceinline__ void load4_cg(const float* p, float (&x)[4]) {
 template <int TL, bool ACC, bool ROWS>
 __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int gen, int flags) {
     constexpr int L = 32 * TL;
-    constexpr int CHA = CHK;  // elements per batch of phase-A loads
+    constexpr int CHA = 2;  // elements per batch of phase-A loads
     const int lane = threadIdx.x & 31;
     const int misc_off = flags >> ROWS_MISC_SHIFT;  // bytes: {mbarrier, counters, row_done, RowConst}
     int* counters = reinterpret_cast<int*>(smem_raw + misc_off + 8);
@@ -1046,8 +1046,9 @@ cudaError_t ensure_constants() {
 
 int tiled_row_warps_for(int warps) {
     if (const char* env = getenv("SFMM_TILED_ROW_WARPS")) return atoi(env);
-    // few warps (small orders): all warps finish the C queue first (measured)
-    return warps >= 8 ? warps / 4 : 0;
+    // measured: no dedicated row warps; every warp takes rows when the C queue is empty
+    (void)warps;
+    return 0;
 }
 
 int tiled_warps_for(int p_rot) {
