@@ -323,11 +323,11 @@ def main():
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                          # dram__bytes_read.sum + dram__bytes_write.sum of translate_tiled_kernel,
                          # one ncu --set full capture of this workload at N=1
-                         # (profiles/ncu_full_translate_tiled_r01.csv): 134 MB read + 121 MB
+                         # (profiles/ncu_full_translate_tiled_r01.csv): 134 MB read + 63 MB
                          # written. Algorithmic: 65 MB sources + 74 MB decomposed shifts + 6 MB
-                         # source indices read, 82 MB partial sums written; the rest is L2
-                         # write-back of register-save stack lines (profiles/ncu_r01_notes.md)
-                         "traffic": 254.6e6 if world == 1 else None,
+                         # source indices read, 82 MB partial sums written (part of them is
+                         # still in L2 when the kernel ends)
+                         "traffic": 196.7e6 if world == 1 else None,
                          "peak_source": "sfmm_measure_fma_peak (DFMA, measured in this run); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
                          "flops_per_translation": flops},
