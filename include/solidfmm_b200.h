@@ -169,9 +169,19 @@ sfmm_status sfmm_m2l_accumulate_host(sfmm_handle* h, const sfmm_plan* plan,
                                      int p_in, int p_out, const void* src_aos,
                                      void* out_aos);
 
+/* Summation unit of sfmm_m2l_accumulate* for this order pair with the kernel the
+ * handle would choose: 64 = pairs j and j+32 of a 64-pair group are added first,
+ * then the 32 sums by the xor butterfly (lane distances 16, 8, 4, 2, 1); 32 or 16 =
+ * xor butterfly over units of that many consecutive pairs; in every case the unit
+ * sums of a target are then added in ascending order. 0 on invalid arguments.
+ * (paper_2202_02847_b200/sharding.py accumulation_tree restates the tree; the
+ * reference has no accumulate mode, pipeline.cpp:258-265 overwrites.) */
+int sfmm_accumulation_unit(const sfmm_handle* h, int p_in, int p_out);
+
 /* Tuning knobs without a reference counterpart. "kernel_variant": 0 = automatic
  * (default), 1 = generic kernel (any order), 2 = tiled kernel (orders <= 20
- * double / <= 18 single; INVALID_ARGUMENT at call time beyond that). */
+ * double / <= 18 single; INVALID_ARGUMENT at call time beyond that), 3 = FP64
+ * tensor-core kernel (double precision, handle order <= 30). */
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value);
 
 /* Measures the FMA-pipe peak (TFLOP/s, 2 flops per FMA) of the handle's device

@@ -54,6 +54,7 @@ _SIGNATURES = {
     "sfmm_m2l_accumulate": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_int64, c_void_p,
                                     c_int64, c_void_p]),
     "sfmm_m2l_accumulate_host": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "sfmm_accumulation_unit": (c_int, [c_void_p, c_int, c_int]),
     "sfmm_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
     "sfmm_measure_fma_peak": (c_int, [c_void_p, POINTER(c_double)]),
     "sfmm_launch_count": (c_int64, [c_void_p]),
@@ -191,6 +192,10 @@ class Handle:
 
     def set_option(self, name: str, value: int) -> None:
         check(self._lib.sfmm_set_option(self._h, name.encode(), value))
+
+    def accumulation_unit(self, p_in: int, p_out: int) -> int:
+        """Summation unit of the accumulate calls (sharding.accumulation_tree `unit`)."""
+        return int(self._lib.sfmm_accumulation_unit(self._h, p_in, p_out))
 
     def measure_fma_peak(self) -> float:
         v = c_double(0)

@@ -106,6 +106,20 @@ sfmm_status upload_tables(sfmm_handle* h, DeviceTables<Real>& t) {
         t.desc[side] = dd;
         t.stream_len[side] = (uint32_t)s.size();
     }
+    // fragment-major copies for the tensor-core kernel (double precision, orders <= 30)
+    if (sizeof(Real) == 8 && h->order <= 30) {
+        for (int side = 0; side < 2; ++side) {
+            const FragSide fs = pack_frags(h->host_tables, side == 1);
+            // zero slack: a product may read a few fragments past its block (masked inputs)
+            std::vector<Real> s(fs.frags.size() + 16 * 32, Real(0));
+            for (size_t i = 0; i < fs.frags.size(); ++i) s[i] = static_cast<Real>(fs.frags[i]);
+            Real* ds = nullptr;
+            CU(cudaMalloc((void**)&ds, s.size() * sizeof(Real)));
+            h->allocations.push_back(ds);
+            CU(cudaMemcpy(ds, s.data(), s.size() * sizeof(Real), cudaMemcpyHostToDevice));
+            t.frags[side] = ds;
+        }
+    }
     std::vector<Real> fac, inv;
     build_faculties<Real>(h->order, fac, inv);
     std::vector<Real> winv(inv);
@@ -139,6 +153,8 @@ sfmm_status check_orders(const sfmm_handle* h, int kind, int p_in, int p_out) {
     if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
     if (h->variant == 2 && std::max(p_in, p_out) > (h->precision == SFMM_F64 ? 20 : 18))
         return fail(SFMM_INVALID_ARGUMENT, "tiled kernel variant does not cover this order");
+    if (h->variant == 3 && (h->precision != SFMM_F64 || h->order > 30))
+        return fail(SFMM_INVALID_ARGUMENT, "mma kernel variant: double precision, handle order <= 30");
     if (kind < 0 || kind > 2) return fail(SFMM_INVALID_ARGUMENT, "unknown translation kind");
     // pipeline.cpp:285-295
     if (p_in < 1 || p_out < 1)
@@ -368,7 +384,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.p_out = p_out;
     a.variant = h->variant;
     // the kernel reduces the lanes of one of ITS groups (32 or 64 pairs) into one partial
-    const int per = kPlanGroup / translate_group_size<Real>(a);
+    const int per = kPlanGroup / translate_group_size<Real>(tables_of<Real>(h), a);
     const int64_t n_partial = plan->n_groups * per;
     Real* partial = nullptr;
     if (n_partial > 0) CU(cudaMallocAsync((void**)&partial, sizeof(Real) * so * n_partial, stream));
@@ -520,6 +536,18 @@ void sfmm_destroy(sfmm_handle* h) {
 
 int sfmm_order(const sfmm_handle* h) { return h ? h->order : 0; }
 int sfmm_device(const sfmm_handle* h) { return h ? h->device : -1; }
+int sfmm_accumulation_unit(const sfmm_handle* h, int p_in, int p_out) {
+    if (!h || p_in < 1 || p_out < 1 || std::max(p_in, p_out) > h->order) return 0;
+    if (h->precision == SFMM_F64) {
+        TranslateArgs<double> a;
+        a.kind = KIND_M2L, a.p_in = p_in, a.p_out = p_out, a.variant = h->variant;
+        return translate_group_size<double>(h->td, a);
+    }
+    TranslateArgs<float> a;
+    a.kind = KIND_M2L, a.p_in = p_in, a.p_out = p_out, a.variant = h->variant;
+    return translate_group_size<float>(h->tf, a);
+}
+
 int64_t sfmm_launch_count(const sfmm_handle* h) { return h ? h->launches.load() : 0; }
 
 sfmm_status sfmm_measure_fma_peak(sfmm_handle* h, double* tflops) {
@@ -536,7 +564,7 @@ sfmm_status sfmm_measure_fma_peak(sfmm_handle* h, double* tflops) {
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
     if (!h || !name) return fail(SFMM_INVALID_ARGUMENT, "null handle or option name");
     if (std::strcmp(name, "kernel_variant") == 0) {
-        if (value < 0 || value > 2) return fail(SFMM_INVALID_ARGUMENT, "kernel_variant must be 0, 1 or 2");
+        if (value < 0 || value > 3) return fail(SFMM_INVALID_ARGUMENT, "kernel_variant must be 0, 1, 2 or 3");
         h->variant = (int)value;
         return SFMM_OK;
     }

@@ -37,6 +37,9 @@ struct DeviceTables {
     const Real* fac = nullptr;   // k!, k <= 2P-2
     const Real* inv = nullptr;   // 1/d!, d < P
     const Real* winv = nullptr;  // (-1)^d / d!, d < P (M2M weights, pipeline.cpp:191-194)
+    // fragment-major swap matrices of the tensor-core kernel (tables.hpp, pack_frags);
+    // double precision handles with order <= 30 only
+    const Real* frags[2] = {nullptr, nullptr};
 };
 
 // One uniform-(p_in, p_out) launch.
@@ -56,7 +59,7 @@ struct TranslateArgs {
     int64_t out_stride = 0;
     const int32_t* src_index = nullptr;  // accumulate mode: source per lane, -1 = idle lane
     const int* fail_flag = nullptr;      // device int; non-zero -> kernel writes nothing
-    int variant = 0;                     // 0 auto, 1 generic kernel, 2 tiled kernel
+    int variant = 0;                     // 0 auto, 1 generic kernel, 2 tiled kernel, 3 mma kernel
     long long* phase_clocks = nullptr;   // optional [8] cycle counters of CTA 0 (tuning aid)
 };
 
@@ -68,9 +71,13 @@ struct LaunchInfo {
     const char* variant = "";
 };
 
-// Group size the kernel chosen for `a` works with (32 generic, 64 tiled).
+// Kernel chosen for `a`: 1 generic, 2 tiled, 3 mma (a.variant forces one when it applies).
 template <typename Real>
-int translate_group_size(const TranslateArgs<Real>& a);
+int translate_variant(const DeviceTables<Real>& t, const TranslateArgs<Real>& a);
+
+// Group size the kernel chosen for `a` works with (32 generic, 64 tiled, 32 / 16 mma).
+template <typename Real>
+int translate_group_size(const DeviceTables<Real>& t, const TranslateArgs<Real>& a);
 
 // Translation kernels. Returns cudaSuccess or the launch error.
 template <typename Real>
@@ -84,6 +91,12 @@ cudaError_t launch_translate_tiled(const DeviceTables<double>& t, const Translat
                                    int sm_count, cudaStream_t stream, LaunchInfo* info);
 cudaError_t launch_translate_tiled(const DeviceTables<float>& t, const TranslateArgs<float>& a,
                                    int sm_count, cudaStream_t stream, LaunchInfo* info);
+
+// Tensor-core kernel (sfmm_mma_f64.cu): double precision, orders <= 30.
+bool mma_supports(const TranslateArgs<double>& a, const DeviceTables<double>& t);
+int mma_group_size(const TranslateArgs<double>& a);
+cudaError_t launch_translate_mma(const DeviceTables<double>& t, const TranslateArgs<double>& a,
+                                 int sm_count, cudaStream_t stream, LaunchInfo* info);
 
 // Measured FMA-pipe peak of the current device in the given precision.
 template <typename Real>

@@ -258,17 +258,55 @@ cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const in
     return cudaGetLastError();
 }
 
+namespace {
+
+// Orders from which the tensor-core kernel wins over the tiled kernel (measured,
+// profiles/): below, the 8 x 4 tiles are mostly padding and the path is HBM-bound anyway.
+constexpr int kMmaMinOrder = 13;
+
+bool mma_ok(const DeviceTables<double>& t, const TranslateArgs<double>& a) { return mma_supports(a, t); }
+bool mma_ok(const DeviceTables<float>&, const TranslateArgs<float>&) { return false; }
+int mma_group(const TranslateArgs<double>& a) { return mma_group_size(a); }
+int mma_group(const TranslateArgs<float>&) { return kLanes; }
+cudaError_t mma_launch(const DeviceTables<double>& t, const TranslateArgs<double>& a, int sm_count,
+                       cudaStream_t stream, LaunchInfo* info) {
+    return launch_translate_mma(t, a, sm_count, stream, info);
+}
+cudaError_t mma_launch(const DeviceTables<float>&, const TranslateArgs<float>&, int, cudaStream_t,
+                       LaunchInfo*) {
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
 template <typename Real>
-int translate_group_size(const TranslateArgs<Real>& a) {
-    return (a.variant != 1 && tiled_supports(a)) ? 64 : kLanes;
+int translate_variant(const DeviceTables<Real>& t, const TranslateArgs<Real>& a) {
+    const int p_rot = std::max(a.p_in, a.p_out);
+    const bool mma = mma_ok(t, a), tiled = tiled_supports(a);
+    switch (a.variant) {
+        case 1: return 1;
+        case 2: return tiled ? 2 : 0;
+        case 3: return mma ? 3 : 0;
+        default: break;
+    }
+    if (mma && (p_rot >= kMmaMinOrder || !tiled)) return 3;
+    return tiled ? 2 : 1;
+}
+
+template <typename Real>
+int translate_group_size(const DeviceTables<Real>& t, const TranslateArgs<Real>& a) {
+    const int v = translate_variant(t, a);
+    return v == 3 ? mma_group(a) : (v == 2 ? 64 : kLanes);
 }
 
 template <typename Real>
 cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Real>& a,
                              int sm_count, cudaStream_t stream, LaunchInfo* info) {
     if (a.n <= 0) return cudaSuccess;
-    if (a.variant != 1 && tiled_supports(a)) return launch_translate_tiled(t, a, sm_count, stream, info);
-    if (a.variant == 2) return cudaErrorInvalidValue;
+    const int v = translate_variant(t, a);
+    if (v == 0) return cudaErrorInvalidValue;
+    if (v == 3) return mma_launch(t, a, sm_count, stream, info);
+    if (v == 2) return launch_translate_tiled(t, a, sm_count, stream, info);
     const int p_rot = std::max(a.p_in, a.p_out);
     const int64_t n_groups = (a.n + kLanes - 1) / kLanes;
     const int limit = smem_optin_limit();
@@ -320,7 +358,9 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
                                                  cudaStream_t);                                 \
     template cudaError_t launch_reduce_groups<Real>(const Real*, int64_t, const int64_t*, int,  \
                                                     int64_t, int, Real*, int64_t, cudaStream_t); \
-    template int translate_group_size<Real>(const TranslateArgs<Real>&);                        \
+    template int translate_variant<Real>(const DeviceTables<Real>&, const TranslateArgs<Real>&); \
+    template int translate_group_size<Real>(const DeviceTables<Real>&,                          \
+                                            const TranslateArgs<Real>&);                        \
     template cudaError_t launch_build_plan<Real>(const int64_t*, const int64_t*, const int32_t*, \
                                                  const int32_t*, const Real*, int64_t, int64_t, \
                                                  int, int32_t*, Real*, Real*, int*, cudaStream_t);     \

@@ -130,6 +130,42 @@ PackedSide pack_side(const SwapTables& t, bool local_side) {
     return out;
 }
 
+FragSide pack_frags(const SwapTables& t, bool local_side) {
+    FragSide out;
+    out.offset.assign(static_cast<size_t>(t.order) * 4 + 1, 0);
+    for (int n = 0; n < t.order; ++n) {
+        const int rows = n + 1;
+        const int cls_size[2] = {n / 2 + 1, (n + 1) / 2};
+        for (int which = 0; which < 2; ++which) {
+            const std::vector<double>& a = which == 0 ? t.f[n] : t.g[n];
+            const int sum_parity = (n + which) & 1;
+            for (int rc = 0; rc < 2; ++rc) {
+                const int cc = (sum_parity - rc) & 1;
+                const int nrows = cls_size[rc], ncols = cls_size[cc];
+                const int KB = (ncols + 3) / 4, MB = (nrows + 7) / 8;
+                out.offset[static_cast<size_t>(n) * 4 + which * 2 + rc] =
+                    static_cast<uint32_t>(out.frags.size() / 32);
+                for (int kb = 0; kb < KB; ++kb)
+                    for (int mb = 0; mb < MB; ++mb)
+                        for (int lane = 0; lane < 32; ++lane) {
+                            const int c = lane >> 2;
+                            const int ii = 8 * mb + (c >> 1) + 4 * (c & 1);
+                            const int kk = 4 * kb + (lane & 3);
+                            double v = 0.0;
+                            if (ii < nrows && kk < ncols) {
+                                const int i = rc + 2 * ii, k = cc + 2 * kk;
+                                v = local_side ? a[static_cast<size_t>(k) * rows + i]
+                                               : a[static_cast<size_t>(i) * rows + k];
+                            }
+                            out.frags.push_back(v);
+                        }
+            }
+        }
+    }
+    out.offset[static_cast<size_t>(t.order) * 4] = static_cast<uint32_t>(out.frags.size() / 32);
+    return out;
+}
+
 size_t packed_prefix_len(int order) {
     size_t len = 0;
     for (int n = 0; n < order; ++n) {

@@ -66,6 +66,28 @@ struct PackedSide {
 // local_side == true:  A = F_n^T, G_n^T (local-type data).
 PackedSide pack_side(const SwapTables& t, bool local_side);
 
+// ---------------------------------------------------------------------------
+// Fragment-major layout for the FP64 tensor-core kernel (sfmm_mma_f64.cu).
+//
+// The kernel evaluates y = A x for 8 translations at a time with
+// mma.sync.m8n8k4.f64: the translations are the 8 rows of the A operand, the
+// swap-matrix block is the B operand (4 inputs x 8 outputs per instruction). One
+// "fragment" is the 32 doubles of one B operand in lane order: lane L holds
+// block(out = sigma(mb, L >> 2), in = 4 kb + (L & 3)), zero outside the block, with
+// the output permutation sigma(mb, c) = 8 mb + (c >> 1) + 4 (c & 1). With this
+// permutation the two accumulator registers of a lane (columns 2q and 2q+1) are
+// outputs 8 mb + q and 8 mb + 4 + q, exactly the A operands of input blocks
+// kb = 2 mb and 2 mb + 1 of the next product: swap -> rotate -> swap chains in
+// registers without any lane exchange. A block's fragments are stored
+// [kb][mb], kb < ceil(ncols / 4), mb < ceil(nrows / 8); blocks in the order of
+// PackedSide::desc (which also gives nrows / ncols; offsets are in fragments
+// and are the same for both sides).
+struct FragSide {
+    std::vector<uint32_t> offset;  // [order * 4 + 1]: first fragment of block n*4 + j
+    std::vector<double> frags;     // 32 doubles per fragment
+};
+FragSide pack_frags(const SwapTables& t, bool local_side);
+
 // Number of stream elements occupied by rows n < order (the stream is ordered
 // by n, so the tables of a lower order are a prefix).
 size_t packed_prefix_len(int order);

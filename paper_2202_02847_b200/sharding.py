@@ -32,12 +32,18 @@ def shard_plan(tgt_ptr: np.ndarray, src_index: np.ndarray, shifts: np.ndarray, r
             np.ascontiguousarray(shifts[p_lo:p_hi]))
 
 
-def accumulation_tree(per_pair: np.ndarray, tgt_ptr: np.ndarray) -> np.ndarray:
+def accumulation_tree(per_pair: np.ndarray, tgt_ptr: np.ndarray, unit: int = 64) -> np.ndarray:
     """The library's fixed summation order for target-owned accumulation, restated
     in numpy; `per_pair` holds one output solid
-    per pair, [pairs, S]. Per target: pairs are cut into groups of 64; inside a
-    group slot j and slot j+32 are added first, then the 32 sums are reduced by the
-    xor butterfly (strides 16, 8, 4, 2, 1); the group sums are added in order."""
+    per pair, [pairs, S]. Per target the pairs are padded with zeros to groups of 64.
+    `unit` is what `sfmm_accumulation_unit` reports for the order pair:
+      64 (tiled kernel): inside a group slot j and slot j+32 are added first, then the
+         32 sums are reduced by the xor butterfly (strides 16, 8, 4, 2, 1);
+      32 / 16 (tensor-core and generic kernels): every `unit` consecutive slots are
+         reduced by the xor butterfly (strides unit/2 ... 1).
+    The unit sums of a target are then added in ascending order."""
+    if unit not in (16, 32, 64):
+        raise ValueError("unit must be 16, 32 or 64")
     n_targets = len(tgt_ptr) - 1
     out = np.zeros((n_targets, per_pair.shape[1]), per_pair.dtype)
     for t in range(n_targets):
@@ -46,10 +52,17 @@ def accumulation_tree(per_pair: np.ndarray, tgt_ptr: np.ndarray) -> np.ndarray:
         for g0 in range(lo, hi, 64):
             blk = np.zeros((64, per_pair.shape[1]), per_pair.dtype)
             blk[:min(64, hi - g0)] = per_pair[g0:min(g0 + 64, hi)]
-            v = blk[:32] + blk[32:]
-            for s in (16, 8, 4, 2, 1):
-                v = v + v[np.arange(32) ^ s]
-            acc = v[0].copy() if acc is None else acc + v[0]
+            if unit == 64:
+                units = [blk[:32] + blk[32:]]
+            else:
+                units = [blk[u:u + unit] for u in range(0, 64, unit)]
+            for v in units:
+                w = len(v)
+                s = w // 2
+                while s >= 1:
+                    v = v + v[np.arange(w) ^ s]
+                    s //= 2
+                acc = v[0].copy() if acc is None else acc + v[0]
         if acc is not None:
             out[t] = acc
     return out

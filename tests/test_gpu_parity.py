@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 GOLDEN = Path(__file__).parent / "golden"
 KINDS = {"m2l": capi.M2L, "m2m": capi.M2M, "l2l": capi.L2L}
-GENERIC, TILED = 1, 2
+GENERIC, TILED, MMA = 1, 2, 3
 
 
 @pytest.fixture(scope="module")
@@ -42,10 +42,10 @@ def run(h, kind, p_in, p_out, src, sh, variant=0):
 
 # ---- random requests, every kind, both kernels -----------------------------
 
-@pytest.mark.parametrize("variant", [GENERIC, TILED], ids=["generic", "tiled"])
+@pytest.mark.parametrize("variant", [GENERIC, TILED, MMA], ids=["generic", "tiled", "mma"])
 def test_random_mixed_orders_f64(oracle, h64, variant):
     rng = np.random.default_rng(7)
-    pmax = 30 if variant == GENERIC else 20
+    pmax = 20 if variant == TILED else 30
     for trial in range(30):
         kind = ("m2l", "m2m", "l2l")[trial % 3]
         p_in, p_out = int(rng.integers(1, pmax + 1)), int(rng.integers(1, pmax + 1))
@@ -76,7 +76,7 @@ def test_group_boundaries(oracle, h64, n):
     rng = np.random.default_rng(n)
     x, sh = random_solids(rng, n, 11), random_shifts(rng, n)
     _, want = oracle.translate("m2l", 11, 9, x, sh)
-    for variant in (GENERIC, TILED):
+    for variant in (GENERIC, TILED, MMA):
         assert bits_equal(run(h64, "m2l", 11, 9, x, sh, variant), want)
 
 
@@ -110,7 +110,7 @@ def test_config2_m2l_f32_p6(oracle, h32):
     assert normalized_error(got[:512], naive) < 1e-5       # north_star FP32 tolerance
 
 
-@pytest.mark.parametrize("variant", [GENERIC, TILED], ids=["generic", "tiled"])
+@pytest.mark.parametrize("variant", [GENERIC, TILED, MMA], ids=["generic", "tiled", "mma"])
 def test_config3_level_accumulation(oracle, h64, variant):
     p = 20
     src, tgt_ptr, idx, sh = workloads.config3(0, (2, 2, 3), p)
@@ -119,13 +119,14 @@ def test_config3_level_accumulation(oracle, h64, variant):
         plan = h64.plan(tgt_ptr, idx, sh, len(src))
         assert plan.pairs == len(idx)
         got = plan.accumulate_host(p, p, src)
+        unit = h64.accumulation_unit(p, p)
         plan.close()
     finally:
         h64.set_option("kernel_variant", 0)
+    assert unit == {GENERIC: 32, TILED: 64, MMA: 32}[variant]
     _, per_pair = oracle.translate("m2l", p, p, src[idx], sh)
-    if variant == TILED:
-        # groups of 64 pairs, documented tree (sharding.accumulation_tree): bit exact
-        assert bits_equal(got, sharding.accumulation_tree(per_pair, tgt_ptr))
+    # the documented tree of the kernel (sharding.accumulation_tree): bit exact
+    assert bits_equal(got, sharding.accumulation_tree(per_pair, tgt_ptr, unit))
     # any summation order of the same terms: 189 terms, a few ulp of the largest
     seq = np.add.reduceat(per_pair, tgt_ptr[:-1], axis=0)
     assert normalized_error(got, seq) < 1e-13
@@ -169,8 +170,10 @@ def test_golden_fixture(h64, h32, path):
         assert bits_equal(out, z["out"])
         return
     p_in, p_out = int(z["p_in"]), int(z["p_out"])
-    for variant in (GENERIC, TILED):
+    for variant in (GENERIC, TILED, MMA):
         if variant == TILED and max(p_in, p_out) > (18 if h is h32 else 20):
+            continue
+        if variant == MMA and h is h32:
             continue
         assert bits_equal(run(h, str(z["kind"]), p_in, p_out, z["src"], z["shifts"], variant), z["out"])
 
@@ -213,7 +216,7 @@ def test_full_config3_level(oracle, h64):
     for t in (0, 777, 4096, 8191):                                              # spot targets, exact
         sl = slice(int(tgt_ptr[t]), int(tgt_ptr[t + 1]))
         _, per_pair = oracle.translate("m2l", p, p, src[idx[sl]], sh[sl])
-        want = sharding.accumulation_tree(per_pair, np.array([0, 189]))
+        want = sharding.accumulation_tree(per_pair, np.array([0, 189]), h64.accumulation_unit(p, p))
         assert bits_equal(out[t], want[0]), t
     # a checksum of checksums: the level is linear in the sources
     out2 = h64.plan(tgt_ptr, idx, sh, len(src)).accumulate_host(p, p, 2.0 * src)
@@ -254,20 +257,22 @@ def test_resident_accumulation_layouts(oracle, h64, h32):
             # Im(C_n^0) is stored as zero by the reduction
             assert bits_equal(got, want), (mode, p)
         assert np.all(want[0] == 0) and np.all(want[4] == 0)                    # targets without pairs
-        # the generic kernel reads the rows layout as well (32-lane groups: another tree)
-        h.set_option("kernel_variant", GENERIC)
-        try:
-            d_out = torch.full((S, ostride), float("nan"), dtype=tdt, device=dev)
-            plan.accumulate_rows(p, p, d_rows.data_ptr(), d_out.data_ptr(), ostride)
-            torch.cuda.synchronize()
-            tol = 1e-13 if dt == np.float64 else 2e-6
-            assert normalized_error(d_out.cpu().numpy()[:, :nt].T.astype(np.float64),
-                                    want.astype(np.float64)) < tol
-        finally:
-            h.set_option("kernel_variant", 0)
-        if dt == np.float64:
-            _, per_pair = oracle.translate("m2l", p, p, src[idx], sh)
-            assert bits_equal(want, sharding.accumulation_tree(per_pair, tgt_ptr))
+        # every kernel reads the rows layout and follows its own documented tree
+        per_pair = oracle.translate("m2l", p, p, src[idx], sh, dt)[1]
+        assert bits_equal(want, sharding.accumulation_tree(per_pair, tgt_ptr, h.accumulation_unit(p, p)))
+        for variant in (GENERIC, TILED, MMA):
+            if variant == MMA and dt != np.float64:
+                continue
+            h.set_option("kernel_variant", variant)
+            try:
+                d_out = torch.full((S, ostride), float("nan"), dtype=tdt, device=dev)
+                plan.accumulate_rows(p, p, d_rows.data_ptr(), d_out.data_ptr(), ostride)
+                torch.cuda.synchronize()
+                unit = h.accumulation_unit(p, p)
+            finally:
+                h.set_option("kernel_variant", 0)
+            assert bits_equal(d_out.cpu().numpy()[:, :nt].T,
+                              sharding.accumulation_tree(per_pair, tgt_ptr, unit)), (variant, p)
         plan.close()
     assert h64.rows_len(20) == 440 and h64.rows_len(1) == 4
 
@@ -282,19 +287,21 @@ def test_accumulation_mixed_orders(oracle, h64):
     tgt_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     idx = rng.integers(0, ns, int(tgt_ptr[-1])).astype(np.int32)
     sh = random_shifts(rng, len(idx), with_axes=False)
-    for p_in, p_out in ((12, 7), (7, 12), (20, 3), (1, 20), (5, 5)):
+    for p_in, p_out in ((12, 7), (7, 12), (20, 3), (1, 20), (5, 5), (24, 12), (13, 27)):
         src = random_solids(rng, ns, p_in)
         plan = h64.plan(tgt_ptr, idx, sh, ns)
         _, per_pair = oracle.translate("m2l", p_in, p_out, src[idx], sh)
-        want = sharding.accumulation_tree(per_pair, tgt_ptr)
-        got = plan.accumulate_host(p_in, p_out, src)
-        assert bits_equal(got, want), (p_in, p_out)
-        h64.set_option("kernel_variant", GENERIC)
-        try:
-            got_g = plan.accumulate_host(p_in, p_out, src)
-        finally:
-            h64.set_option("kernel_variant", 0)
-        assert normalized_error(got_g, want) < 1e-13, (p_in, p_out)
+        for variant in (0, GENERIC, TILED, MMA):
+            if variant == TILED and max(p_in, p_out) > 20:
+                continue
+            h64.set_option("kernel_variant", variant)
+            try:
+                got = plan.accumulate_host(p_in, p_out, src)
+                unit = h64.accumulation_unit(p_in, p_out)
+            finally:
+                h64.set_option("kernel_variant", 0)
+            want = sharding.accumulation_tree(per_pair, tgt_ptr, unit)
+            assert bits_equal(got, want), (p_in, p_out, variant)
         plan.close()
 
 

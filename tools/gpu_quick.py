@@ -12,6 +12,8 @@ bad = 0
 import os
 variant = int(os.environ.get("VARIANT", "0"))
 for dt, prec, pmax in ((np.float64, capi.F64, 30 if variant != 2 else 20), (np.float32, capi.F32, 18)):
+    if variant == 3 and prec == capi.F32:
+        continue
     h = capi.Handle(prec, pmax)
     h.set_option("kernel_variant", variant)
     for trial in range(36):

@@ -16,6 +16,8 @@ prec = capi.F32 if (len(sys.argv) > 6 and sys.argv[6] == "f32") else capi.F64
 dt = torch.float32 if prec == capi.F32 else torch.float64
 dev = torch.device("cuda", 0)
 h = capi.Handle(prec, P)
+import os as _os0
+h.set_option("kernel_variant", int(_os0.environ.get("VARIANT", "0")))
 peak = h.measure_fma_peak()
 S = P * (P + 1)
 stream = torch.cuda.current_stream().cuda_stream
