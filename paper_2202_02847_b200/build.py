@@ -36,6 +36,8 @@ NVCC_FLAGS = [
 # tuning build: per-phase cycle counters in the tiled kernel (tools/perf_probe.py PHASES=1)
 if os.environ.get("SFMM_PHASE_CLOCKS"):
     NVCC_FLAGS.append("-DSFMM_PHASE_CLOCKS")
+# tuning build: extra -D definitions (e.g. SFMM_DEFS="-DSFMM_MMA_NE=8")
+NVCC_FLAGS += os.environ.get("SFMM_DEFS", "").split()
 
 
 def nvcc_path() -> str:

@@ -64,7 +64,9 @@ _lib = None
 
 
 def library_path() -> Path:
-    return _build.LIB_PATH
+    # SFMM_LIB: a tuning build of the same library (tools/, never the tests)
+    import os
+    return Path(os.environ["SFMM_LIB"]) if os.environ.get("SFMM_LIB") else _build.LIB_PATH
 
 
 def load_library() -> ctypes.CDLL:
