@@ -260,9 +260,12 @@ cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const in
 
 namespace {
 
-// Orders from which the tensor-core kernel wins over the tiled kernel (measured,
-// profiles/): below, the 8 x 4 tiles are mostly padding and the path is HBM-bound anyway.
-constexpr int kMmaMinOrder = 13;
+// Orders from which the tensor-core kernel is the automatic choice (measured, profiles/
+// ncu_r02_notes.md): up to order 20 the tiled DFMA kernel is 15-17 % faster (the 8 x 4 tiles
+// of m8n8k4 are half padding at the class sizes 9 and 10, and DMMA shares its issue port with
+// the FP64 and integer multiply-add instructions around it); from order 21 on the tiled
+// kernel does not apply and the tensor-core kernel is ~5x the generic kernel.
+constexpr int kMmaMinOrder = 21;
 
 bool mma_ok(const DeviceTables<double>& t, const TranslateArgs<double>& a) { return mma_supports(a, t); }
 bool mma_ok(const DeviceTables<float>&, const TranslateArgs<float>&) { return false; }

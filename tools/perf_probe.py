@@ -69,7 +69,7 @@ if pc is not None:
     v = pc.cpu().numpy().astype(float); tot = v.sum()
     names = ["G geometry", "A load+rot", "B fwd swaps", "Z z-step", "C bwd swaps", "D rot+store"]
     if _os0.environ.get("VARIANT") == "3":
-        names = ["M wait A", "B fwd swaps", "Z z-step", "C bwd swaps", "E wait C", "E work"]
+        names = ["rows only", "P1 B", "P2 Z+D", "P3 C+A", "-", "-"]
     print("raw", [int(x) for x in v])
     print("phase cycles of CTA 0 (all launches):", ", ".join(f"{n}: {100*x/tot:.1f}%" for n, x in zip(names, v)), f"total {tot:.3e}")
 tps = units / (best * 1e-3)
