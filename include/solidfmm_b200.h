@@ -189,6 +189,11 @@ sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value);
  * use it as the compute-roofline denominator. */
 sfmm_status sfmm_measure_fma_peak(sfmm_handle* h, double* tflops);
 
+/* The same for the FP64 tensor-core instruction (mma.m8n8k4.f64, 512 flops per warp
+ * instruction). Both run on one pipe; benchmarks take the larger of the two as the
+ * FP64 roofline and report both. */
+sfmm_status sfmm_measure_dmma_peak(sfmm_handle* h, double* tflops);
+
 /* Number of kernel launches this handle has issued (bench.py gpu_launches). */
 int64_t sfmm_launch_count(const sfmm_handle* h);
 

@@ -57,6 +57,7 @@ _SIGNATURES = {
     "sfmm_accumulation_unit": (c_int, [c_void_p, c_int, c_int]),
     "sfmm_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
     "sfmm_measure_fma_peak": (c_int, [c_void_p, POINTER(c_double)]),
+    "sfmm_measure_dmma_peak": (c_int, [c_void_p, POINTER(c_double)]),
     "sfmm_launch_count": (c_int64, [c_void_p]),
 }
 
@@ -202,6 +203,11 @@ class Handle:
     def measure_fma_peak(self) -> float:
         v = c_double(0)
         check(self._lib.sfmm_measure_fma_peak(self._h, ctypes.byref(v)))
+        return v.value
+
+    def measure_dmma_peak(self) -> float:
+        v = c_double(0)
+        check(self._lib.sfmm_measure_dmma_peak(self._h, ctypes.byref(v)))
         return v.value
 
     def swap_tables(self, n: int):

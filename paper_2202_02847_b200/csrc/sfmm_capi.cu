@@ -561,6 +561,14 @@ sfmm_status sfmm_measure_fma_peak(sfmm_handle* h, double* tflops) {
     return SFMM_OK;
 }
 
+sfmm_status sfmm_measure_dmma_peak(sfmm_handle* h, double* tflops) {
+    if (!h || !tflops) return fail(SFMM_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(h->device);
+    CU(measure_dmma_peak(h->sm_count, tflops));
+    h->launches += 4;
+    return SFMM_OK;
+}
+
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
     if (!h || !name) return fail(SFMM_INVALID_ARGUMENT, "null handle or option name");
     if (std::strcmp(name, "kernel_variant") == 0) {

@@ -102,6 +102,9 @@ cudaError_t launch_translate_mma(const DeviceTables<double>& t, const TranslateA
 template <typename Real>
 cudaError_t measure_fma_peak(int sm_count, double* tflops);
 
+// Measured FP64 tensor-core (mma.m8n8k4.f64) peak of the current device.
+cudaError_t measure_dmma_peak(int sm_count, double* tflops);
+
 // Zero-shift scan: sets *flag (device int) to 1 when any |shift| < min normal.
 template <typename Real>
 cudaError_t launch_check_shifts(const Real* shifts, int64_t n, int* flag, cudaStream_t stream);

@@ -135,6 +135,24 @@ __global__ void fma_peak_kernel(Real* out, int iters, Real a, Real b) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// FP64 tensor-core peak probe: back-to-back mma.m8n8k4.f64 on 8 accumulator pairs per warp
+__global__ void dmma_peak_kernel(double* out, int iters, double a, double b) {
+    double d[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j][0] = d[j][1] = double(threadIdx.x + j);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(d[j][0]), "+d"(d[j][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += d[j][0] + d[j][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int g_smem_optin = -1;
 
 int smem_optin_limit() {
@@ -176,6 +194,34 @@ cudaError_t measure_fma_peak(int sm_count, double* tflops) {
     *tflops = 2.0 * 64 * iters * (double)grid * block / (best * 1e-3) * 1e-12;
     return cudaGetLastError();
 }
+cudaError_t measure_dmma_peak(int sm_count, double* tflops) {
+    const int block = 256, grid = sm_count * 2, iters = 8192;
+    double* out = nullptr;
+    cudaError_t e = cudaMalloc((void**)&out, sizeof(double) * (size_t)grid * block);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 4; ++r) {
+        cudaEventRecord(e0);
+        dmma_peak_kernel<<<grid, block>>>(out, iters, 1.0000001, 1e-9);
+        cudaEventRecord(e1);
+        e = cudaEventSynchronize(e1);
+        if (e != cudaSuccess) break;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (e != cudaSuccess) return e;
+    // 8 x 8 x 4 multiply-adds per warp instruction
+    *tflops = 2.0 * 256 * 8 * iters * (double)grid * (block / 32) / (best * 1e-3) * 1e-12;
+    return cudaGetLastError();
+}
+
 template cudaError_t measure_fma_peak<double>(int, double*);
 template cudaError_t measure_fma_peak<float>(int, double*);
 
