@@ -181,7 +181,8 @@ int sfmm_accumulation_unit(const sfmm_handle* h, int p_in, int p_out);
 /* Tuning knobs without a reference counterpart. "kernel_variant": 0 = automatic
  * (default), 1 = generic kernel (any order), 2 = tiled kernel (orders <= 20
  * double / <= 18 single; INVALID_ARGUMENT at call time beyond that), 3 = FP64
- * tensor-core kernel (double precision, handle order <= 30). */
+ * tensor-core kernel (double precision, handle order <= 30), 4 = small-order kernel
+ * (same order <= 8, independent translations). */
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value);
 
 /* Measures the FMA-pipe peak (TFLOP/s, 2 flops per FMA) of the handle's device

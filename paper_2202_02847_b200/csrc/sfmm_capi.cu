@@ -155,6 +155,8 @@ sfmm_status check_orders(const sfmm_handle* h, int kind, int p_in, int p_out) {
         return fail(SFMM_INVALID_ARGUMENT, "tiled kernel variant does not cover this order");
     if (h->variant == 3 && (h->precision != SFMM_F64 || h->order > 30))
         return fail(SFMM_INVALID_ARGUMENT, "mma kernel variant: double precision, handle order <= 30");
+    if (h->variant == 4 && (p_in != p_out || p_in > 8))
+        return fail(SFMM_INVALID_ARGUMENT, "small kernel variant: same order, at most 8");
     if (kind < 0 || kind > 2) return fail(SFMM_INVALID_ARGUMENT, "unknown translation kind");
     // pipeline.cpp:285-295
     if (p_in < 1 || p_out < 1)
@@ -572,7 +574,7 @@ sfmm_status sfmm_measure_dmma_peak(sfmm_handle* h, double* tflops) {
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
     if (!h || !name) return fail(SFMM_INVALID_ARGUMENT, "null handle or option name");
     if (std::strcmp(name, "kernel_variant") == 0) {
-        if (value < 0 || value > 3) return fail(SFMM_INVALID_ARGUMENT, "kernel_variant must be 0, 1, 2 or 3");
+        if (value < 0 || value > 4) return fail(SFMM_INVALID_ARGUMENT, "kernel_variant must be 0..4");
         h->variant = (int)value;
         return SFMM_OK;
     }

@@ -59,7 +59,7 @@ struct TranslateArgs {
     int64_t out_stride = 0;
     const int32_t* src_index = nullptr;  // accumulate mode: source per lane, -1 = idle lane
     const int* fail_flag = nullptr;      // device int; non-zero -> kernel writes nothing
-    int variant = 0;                     // 0 auto, 1 generic kernel, 2 tiled kernel, 3 mma kernel
+    int variant = 0;                     // 0 auto, 1 generic, 2 tiled, 3 mma, 4 small-order kernel
     long long* phase_clocks = nullptr;   // optional [8] cycle counters of CTA 0 (tuning aid)
 };
 
@@ -71,7 +71,8 @@ struct LaunchInfo {
     const char* variant = "";
 };
 
-// Kernel chosen for `a`: 1 generic, 2 tiled, 3 mma (a.variant forces one when it applies).
+// Kernel chosen for `a`: 1 generic, 2 tiled, 3 mma, 4 small (a.variant forces one when it
+// applies, 0 = it does not).
 template <typename Real>
 int translate_variant(const DeviceTables<Real>& t, const TranslateArgs<Real>& a);
 
@@ -97,6 +98,12 @@ bool mma_supports(const TranslateArgs<double>& a, const DeviceTables<double>& t)
 int mma_group_size(const TranslateArgs<double>& a);
 cudaError_t launch_translate_mma(const DeviceTables<double>& t, const TranslateArgs<double>& a,
                                  int sm_count, cudaStream_t stream, LaunchInfo* info);
+
+// Small-order kernel (sfmm_small.cu): same-order independent translations, P <= 8, SoA.
+bool small_supports(const TranslateArgs<double>& a);
+bool small_supports(const TranslateArgs<float>& a);
+cudaError_t launch_translate_small(const TranslateArgs<double>& a, cudaStream_t stream, LaunchInfo* info);
+cudaError_t launch_translate_small(const TranslateArgs<float>& a, cudaStream_t stream, LaunchInfo* info);
 
 // Measured FMA-pipe peak of the current device in the given precision.
 template <typename Real>

@@ -332,12 +332,15 @@ template <typename Real>
 int translate_variant(const DeviceTables<Real>& t, const TranslateArgs<Real>& a) {
     const int p_rot = std::max(a.p_in, a.p_out);
     const bool mma = mma_ok(t, a), tiled = tiled_supports(a);
+    const bool small = small_supports(a);
     switch (a.variant) {
         case 1: return 1;
         case 2: return tiled ? 2 : 0;
         case 3: return mma ? 3 : 0;
+        case 4: return small ? 4 : 0;
         default: break;
     }
+    if (small) return 4;
     if (mma && (p_rot >= kMmaMinOrder || !tiled)) return 3;
     return tiled ? 2 : 1;
 }
@@ -354,6 +357,7 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
     if (a.n <= 0) return cudaSuccess;
     const int v = translate_variant(t, a);
     if (v == 0) return cudaErrorInvalidValue;
+    if (v == 4) return launch_translate_small(a, stream, info);
     if (v == 3) return mma_launch(t, a, sm_count, stream, info);
     if (v == 2) return launch_translate_tiled(t, a, sm_count, stream, info);
     const int p_rot = std::max(a.p_in, a.p_out);

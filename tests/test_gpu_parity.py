@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 GOLDEN = Path(__file__).parent / "golden"
 KINDS = {"m2l": capi.M2L, "m2m": capi.M2M, "l2l": capi.L2L}
-GENERIC, TILED, MMA = 1, 2, 3
+GENERIC, TILED, MMA, SMALL = 1, 2, 3, 4
 
 
 @pytest.fixture(scope="module")
@@ -69,6 +69,28 @@ def test_random_mixed_orders_f32(oracle, h32, variant):
         st, want = oracle.translate(kind, p_in, p_out, x, sh, np.float32)
         assert st == 0
         assert bits_equal(run(h32, kind, p_in, p_out, x, sh, variant), want), (kind, p_in, p_out, n)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_small_order_kernel(oracle, h64, h32, prec):
+    """The register-resident kernel (same order <= 8, the automatic choice there): every
+    order, every kind, both precisions, bit for bit; the other kernels agree with it."""
+    rng = np.random.default_rng(11)
+    h, dt = (h64, np.float64) if prec == "f64" else (h32, np.float32)
+    for p in range(1, 9):
+        for kind in ("m2l", "m2m", "l2l"):
+            n = int(rng.integers(1, 400))
+            x = random_solids(rng, n, p, dt, 0.05 if dt == np.float32 else 1.0)
+            sh = random_shifts(rng, n, dtype=dt)
+            st, want = oracle.translate(kind, p, p, x, sh, dt)
+            assert st == 0
+            assert bits_equal(run(h, kind, p, p, x, sh, SMALL), want), (kind, p, n)
+            assert bits_equal(run(h, kind, p, p, x, sh, 0), want), (kind, p, n)
+            assert bits_equal(run(h, kind, p, p, x, sh, TILED), want), (kind, p, n)
+    with pytest.raises(capi.InvalidArgument):
+        run(h, "m2l", 9, 9, random_solids(rng, 4, 9, dt), random_shifts(rng, 4, dtype=dt), SMALL)
+    with pytest.raises(capi.InvalidArgument):
+        run(h, "m2l", 6, 5, random_solids(rng, 4, 6, dt), random_shifts(rng, 4, dtype=dt), SMALL)
 
 
 @pytest.mark.parametrize("n", [1, 31, 32, 33, 63, 64, 65, 129])
@@ -176,6 +198,8 @@ def test_golden_fixture(h64, h32, path):
         if variant == MMA and h is h32:
             continue
         assert bits_equal(run(h, str(z["kind"]), p_in, p_out, z["src"], z["shifts"], variant), z["out"])
+    if p_in == p_out and p_in <= 8:
+        assert bits_equal(run(h, str(z["kind"]), p_in, p_out, z["src"], z["shifts"], SMALL), z["out"])
 
 
 # ---- full-size runs: size-independent properties ---------------------------
