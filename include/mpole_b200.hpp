@@ -24,6 +24,7 @@
 #include <complex>
 #include <cstddef>
 #include <cstdint>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -221,6 +222,10 @@ void run_batch(sfmm_kind kind, const operator_data<Real>& ops,
         const int needed = std::max(p_in[i], p_out[i]);
         if (needed > ops.order()) throw std::invalid_argument("translation order exceeds operator data order");
         if (needed > ws.max_order()) throw std::invalid_argument("translation order exceeds workspace capacity");
+        // per request, in the reference's order (pipeline.cpp:282-298): a zero shift in an
+        // earlier request wins over a bad order in a later one
+        if (std::hypot(req.shift.x, req.shift.y, req.shift.z) < std::numeric_limits<Real>::min())
+            throw std::domain_error("translation with zero shift vector");
         in_off[i] = static_cast<int64_t>(in_len);
         out_off[i] = static_cast<int64_t>(out_len);
         in_len += solid_size(p_in[i]);

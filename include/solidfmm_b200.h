@@ -104,13 +104,18 @@ sfmm_status sfmm_translate_host_mixed(sfmm_handle* h, sfmm_kind kind, int64_t n,
  * DOMAIN_ERROR, with SFMM_ASYNC_STATUS it returns at once and the outcome is
  * read later with sfmm_stream_status(). */
 enum { SFMM_SYNC_STATUS = 0, SFMM_ASYNC_STATUS = 1 };
+/* The host-buffer entry points (sfmm_translate_host, _mixed, sfmm_plan_create,
+ * sfmm_m2l_accumulate_host) run on a private non-blocking stream per calling thread and
+ * device: concurrent callers do not serialise on the legacy default stream. */
 sfmm_status sfmm_translate_soa(sfmm_handle* h, sfmm_kind kind, int64_t n,
                                int p_in, int p_out, const void* d_in,
                                int64_t in_stride, const void* d_shifts,
                                void* d_out, int64_t out_stride, void* stream,
                                int flags);
-/* Synchronises `stream` and reports the status of the SoA calls enqueued with
- * SFMM_ASYNC_STATUS since the last query (DOMAIN_ERROR if any scan failed). */
+/* Synchronises `stream` and reports the status of the SoA calls enqueued ON THAT STREAM
+ * with SFMM_ASYNC_STATUS since its last query (DOMAIN_ERROR if any scan failed). Calls
+ * issued on other streams keep their status until their own stream is queried. A handle
+ * tracks up to 256 unqueried calls; beyond that a call reports synchronously. */
 sfmm_status sfmm_stream_status(sfmm_handle* h, void* stream);
 
 /* AoS <-> SoA repacking on the device (batch of n solids of order p). */
@@ -144,9 +149,9 @@ sfmm_status sfmm_plan_create(sfmm_handle* h, int64_t n_targets,
                              const int64_t* tgt_ptr, const int32_t* src_index,
                              const void* shifts, int64_t n_sources,
                              sfmm_plan** out);
-/* Frees the plan behind the work already enqueued on the default stream and on
- * blocking streams; callers that launch on non-blocking streams synchronise
- * them first. */
+/* Frees the plan, ordered behind the most recent accumulate call that used it (on that
+ * call's stream). Callers that use one plan on several streams at once synchronise the
+ * other streams first. */
 void sfmm_plan_destroy(sfmm_plan* plan);
 int64_t sfmm_plan_pairs(const sfmm_plan* plan);
 

@@ -145,6 +145,15 @@ def solid_size(order: int) -> int:
     return order * (order + 1)
 
 
+def _check_buffer(a: np.ndarray, dtype, min_size: int, what: str) -> None:
+    """A caller-supplied host array the C side reads or writes `min_size` elements of."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.dtype(dtype) or not a.flags.c_contiguous \
+            or a.size < min_size:
+        raise InvalidArgument(INVALID_ARGUMENT,
+                              f"{what}: need a C-contiguous {np.dtype(dtype).name} array of at least "
+                              f"{min_size} elements")
+
+
 def _ptr(a) -> c_void_p:
     """Host numpy array, raw address (int) or None -> void*."""
     if a is None:
@@ -231,6 +240,9 @@ class Handle:
         n = shifts.shape[0] if shifts.ndim == 2 else shifts.size // 3
         if out is None:
             out = np.empty((n, solid_size(max(p_out, 1))), self.dtype)
+        _check_buffer(out, self.dtype, n * solid_size(max(p_out, 1)), "out")
+        if src.size < n * solid_size(max(p_in, 1)):
+            raise InvalidArgument(INVALID_ARGUMENT, "src holds fewer than n solids of order p_in")
         check(self._lib.sfmm_translate_host(self._h, kind, n, p_in, p_out, _ptr(src),
                                             _ptr(shifts), _ptr(out)))
         return out
@@ -242,6 +254,16 @@ class Handle:
         in_off = np.ascontiguousarray(in_off, np.int64)
         out_off = np.ascontiguousarray(out_off, np.int64)
         shifts = np.ascontiguousarray(shifts, self.dtype)
+        src = np.ascontiguousarray(src, self.dtype)
+        n = len(p_in)
+        if not (len(p_out) == len(in_off) == len(out_off) == n) or shifts.size < 3 * n:
+            raise InvalidArgument(INVALID_ARGUMENT, "per-request arrays of different lengths")
+        if n:
+            sizes_in = p_in.astype(np.int64) * (p_in + 1)
+            sizes_out = p_out.astype(np.int64) * (p_out + 1)
+            if np.any(in_off < 0) or np.any(out_off < 0) or np.any(in_off + sizes_in > src.size):
+                raise InvalidArgument(INVALID_ARGUMENT, "a source lies outside src")
+            _check_buffer(out, self.dtype, int((out_off + sizes_out).max()), "out")
         check(self._lib.sfmm_translate_host_mixed(self._h, kind, len(p_in), _ptr(p_in),
                                                   _ptr(p_out), _ptr(src), _ptr(in_off),
                                                   _ptr(shifts), _ptr(out), _ptr(out_off)))
@@ -321,6 +343,9 @@ class Plan:
         src = np.ascontiguousarray(src, self._handle.dtype)
         if out is None:
             out = np.empty((self.n_targets, solid_size(p_out)), self._handle.dtype)
+        _check_buffer(out, self._handle.dtype, self.n_targets * solid_size(p_out), "out")
+        if src.size < self.n_sources * solid_size(p_in):
+            raise InvalidArgument(INVALID_ARGUMENT, "src holds fewer than n_sources solids of order p_in")
         check(self._lib.sfmm_m2l_accumulate_host(self._handle._h, self._p, p_in, p_out, _ptr(src),
                                                  _ptr(out)))
         return out

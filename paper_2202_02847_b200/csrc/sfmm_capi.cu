@@ -45,7 +45,36 @@ struct DeviceGuard {
     }
 };
 
+// Stream of the host-buffer entry points: one non-blocking stream per calling thread and
+// device, so that concurrent callers (one workspace per thread in the reference,
+// pipeline.hpp:30-45) neither serialise on the legacy default stream nor on each other.
+cudaStream_t host_stream(int device) {
+    thread_local std::vector<std::pair<int, cudaStream_t>> cache;
+    for (const auto& e : cache)
+        if (e.first == device) return e.second;
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) s = nullptr;
+    cache.emplace_back(device, s);
+    return s;
+}
+
+// Stream-ordered device allocation that is released on every exit path.
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s;
+    explicit DevBuf(cudaStream_t stream) : s(stream) {}
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s); }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
 constexpr int kFlagSlots = 256;
+constexpr int64_t kHostChunk = 1 << 20;  // translations per staging chunk of the host path
 constexpr int kPlanGroup = 64;  // pairs of one target are padded to multiples of this
 
 int64_t round_up32(int64_t n) { return (n + 31) / 32 * 32; }
@@ -65,10 +94,17 @@ struct sfmm_handle {
     std::vector<void*> allocations;
     int* d_flags = nullptr;
     int* h_flags = nullptr;  // pinned
-    std::atomic<unsigned> flag_cursor{0};
     std::atomic<int64_t> launches{0};
+    // zero-shift flags of the device entry points: a slot belongs to one call until its
+    // result has been read (synchronous calls: at once; SFMM_ASYNC_STATUS calls: by
+    // sfmm_stream_status on the stream they were issued on)
+    struct Pending {
+        int slot;
+        cudaStream_t stream;
+    };
     std::mutex async_mutex;
-    std::vector<int> async_slots;
+    std::vector<int> free_slots;
+    std::vector<Pending> pending;
     int variant = 0;
     long long* d_phase_clocks = nullptr;  // set by the "phase_clocks" option
 };
@@ -80,6 +116,7 @@ struct sfmm_plan {
     int32_t* d_src_index = nullptr; // [n_groups * 64], -1 = idle lane
     void* d_shifts = nullptr;       // [n_groups * 64][3]
     void* d_angles = nullptr;       // [6][n_groups * 64]: decomposed shifts (TranslateArgs::angles)
+    cudaStream_t last_stream = nullptr;  // stream of the most recent accumulate call (destroy order)
 };
 
 namespace {
@@ -175,6 +212,18 @@ bool host_shift_degenerate(const Real* r) {
     return std::hypot(r[0], r[1], r[2]) < mn;
 }
 
+int acquire_slot(sfmm_handle* h) {
+    std::lock_guard<std::mutex> lk(h->async_mutex);
+    if (h->free_slots.empty()) return -1;
+    const int slot = h->free_slots.back();
+    h->free_slots.pop_back();
+    return slot;
+}
+void release_slot(sfmm_handle* h, int slot) {
+    std::lock_guard<std::mutex> lk(h->async_mutex);
+    h->free_slots.push_back(slot);
+}
+
 template <typename Real>
 sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, int p_out,
                                const Real* d_in, int64_t in_stride, const Real* d_shifts,
@@ -182,11 +231,21 @@ sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, in
                                bool skip_scan) {
     int slot = -1;
     int* d_flag = nullptr;
+    DevBuf spare(stream);  // flag of a call that finds every slot waiting for its query
     if (!skip_scan) {
-        slot = (int)(h->flag_cursor.fetch_add(1) % kFlagSlots);
-        d_flag = h->d_flags + slot;
-        CU(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
-        CU(launch_check_shifts<Real>(d_shifts, n, d_flag, stream));
+        slot = acquire_slot(h);
+        if (slot >= 0) {
+            d_flag = h->d_flags + slot;
+        } else {
+            CU(spare.alloc(sizeof(int)));
+            d_flag = spare.as<int>();
+        }
+        cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), stream);
+        if (e == cudaSuccess) e = launch_check_shifts<Real>(d_shifts, n, d_flag, stream);
+        if (e != cudaSuccess) {
+            if (slot >= 0) release_slot(h, slot);
+            return cuda_fail(e, "zero-shift scan");
+        }
         h->launches += 1;
     }
     TranslateArgs<Real> a;
@@ -203,17 +262,30 @@ sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, in
     a.variant = h->variant;
     a.phase_clocks = h->d_phase_clocks;
     LaunchInfo info;
-    CU(launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info));
+    cudaError_t e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
+    if (e != cudaSuccess) {
+        if (slot >= 0) {
+            cudaStreamSynchronize(stream);  // the scan may still write the slot
+            release_slot(h, slot);
+        }
+        return cuda_fail(e, "launch_translate");
+    }
     h->launches += info.launches;
     if (skip_scan) return SFMM_OK;
-    if (flags & SFMM_ASYNC_STATUS) {
+    if ((flags & SFMM_ASYNC_STATUS) && slot >= 0) {
         std::lock_guard<std::mutex> lk(h->async_mutex);
-        h->async_slots.push_back(slot);
+        h->pending.push_back({slot, stream});
         return SFMM_OK;
     }
-    CU(cudaMemcpyAsync(h->h_flags + slot, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CU(cudaStreamSynchronize(stream));
-    if (h->h_flags[slot]) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
+    // synchronous status (also when all slots are taken: the call then reports at once)
+    int value = 0;
+    int* dst = slot >= 0 ? h->h_flags + slot : &value;
+    e = cudaMemcpyAsync(dst, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    const int bad = *dst;
+    if (slot >= 0) release_slot(h, slot);
+    if (e != cudaSuccess) return cuda_fail(e, "zero-shift status");
+    if (bad) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
     return SFMM_OK;
 }
 
@@ -223,35 +295,33 @@ sfmm_status translate_host_impl(sfmm_handle* h, int kind, int64_t n, int p_in, i
     for (int64_t i = 0; i < n; ++i)
         if (host_shift_degenerate(shifts + 3 * i))
             return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
-    const int64_t si = solid_len(p_in), so = solid_len(p_out), stride = round_up32(n);
-    cudaStream_t stream = nullptr;
-    Real *d_in_aos = nullptr, *d_in = nullptr, *d_sh = nullptr, *d_out = nullptr,
-         *d_out_aos = nullptr;
+    const int64_t si = solid_len(p_in), so = solid_len(p_out);
+    // staged in chunks: the device scratch stays bounded however large the batch is, and
+    // everything is ordered on one stream with a single synchronisation at the end
+    const int64_t chunk = std::min(n, kHostChunk), stride = round_up32(chunk);
+    cudaStream_t stream = host_stream(h->device);
+    DevBuf d_in_aos(stream), d_in(stream), d_sh(stream), d_out(stream), d_out_aos(stream);
     const size_t es = sizeof(Real);
-    CU(cudaMallocAsync((void**)&d_in_aos, es * si * n, stream));
-    CU(cudaMallocAsync((void**)&d_in, es * si * stride, stream));
-    CU(cudaMallocAsync((void**)&d_sh, es * 3 * n, stream));
-    CU(cudaMallocAsync((void**)&d_out, es * so * stride, stream));
-    CU(cudaMallocAsync((void**)&d_out_aos, es * so * n, stream));
-    CU(cudaMemcpyAsync(d_in_aos, in, es * si * n, cudaMemcpyHostToDevice, stream));
-    CU(cudaMemcpyAsync(d_sh, shifts, es * 3 * n, cudaMemcpyHostToDevice, stream));
-    CU(launch_pack_soa<Real>(d_in_aos, d_in, n, p_in, stride, stream));
-    sfmm_status st = translate_soa_impl<Real>(h, kind, n, p_in, p_out, d_in, stride, d_sh, d_out,
-                                              stride, stream, 0, /*skip_scan=*/true);
-    if (st == SFMM_OK) {
-        cudaError_t e = launch_unpack_soa<Real>(d_out, d_out_aos, n, p_out, stride, stream);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(out, d_out_aos, es * so * n, cudaMemcpyDeviceToHost, stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) st = cuda_fail(e, "translate_host");
+    CU(d_in_aos.alloc(es * si * chunk));
+    CU(d_in.alloc(es * si * stride));
+    CU(d_sh.alloc(es * 3 * chunk));
+    CU(d_out.alloc(es * so * stride));
+    CU(d_out_aos.alloc(es * so * chunk));
+    for (int64_t lo = 0; lo < n; lo += chunk) {
+        const int64_t m = std::min(chunk, n - lo);
+        CU(cudaMemcpyAsync(d_in_aos.p, in + lo * si, es * si * m, cudaMemcpyHostToDevice, stream));
+        CU(cudaMemcpyAsync(d_sh.p, shifts + 3 * lo, es * 3 * m, cudaMemcpyHostToDevice, stream));
+        CU(launch_pack_soa<Real>(d_in_aos.as<Real>(), d_in.as<Real>(), m, p_in, stride, stream));
+        const sfmm_status st =
+            translate_soa_impl<Real>(h, kind, m, p_in, p_out, d_in.as<Real>(), stride, d_sh.as<Real>(),
+                                     d_out.as<Real>(), stride, stream, 0, /*skip_scan=*/true);
+        if (st != SFMM_OK) return st;
+        CU(launch_unpack_soa<Real>(d_out.as<Real>(), d_out_aos.as<Real>(), m, p_out, stride, stream));
+        CU(cudaMemcpyAsync(out + lo * so, d_out_aos.p, es * so * m, cudaMemcpyDeviceToHost, stream));
         h->launches += 2;
     }
-    cudaFreeAsync(d_in_aos, stream);
-    cudaFreeAsync(d_in, stream);
-    cudaFreeAsync(d_sh, stream);
-    cudaFreeAsync(d_out, stream);
-    cudaFreeAsync(d_out_aos, stream);
-    return st;
+    CU(cudaStreamSynchronize(stream));
+    return SFMM_OK;
 }
 
 template <typename Real>
@@ -272,35 +342,63 @@ sfmm_status translate_host_mixed_impl(sfmm_handle* h, int kind, int64_t n, const
         if (p_in[a] != p_in[b]) return p_in[a] < p_in[b];
         return p_out[a] < p_out[b];
     });
-    // sources are staged before any output is written, so an output may alias
-    // its own source even when the order changes (pipeline.cpp:312-324)
-    std::vector<std::vector<Real>> stage_in, stage_sh;
+    // One upload, one launch sequence per order pair, one download. The sources are staged
+    // (sorted by order pair) before any output is written, so an output may alias its own
+    // source even when the order changes (pipeline.cpp:312-324).
+    std::vector<int64_t> in_pos((size_t)n), out_pos((size_t)n);
+    int64_t in_len = 0, out_len = 0, max_group = 0, max_si = 0, max_so = 0;
     std::vector<std::pair<int64_t, int64_t>> ranges;
     for (int64_t i = 0; i < n;) {
         int64_t j = i;
         while (j < n && p_in[idx[j]] == p_in[idx[i]] && p_out[idx[j]] == p_out[idx[i]]) ++j;
-        const int64_t si = solid_len(p_in[idx[i]]);
-        std::vector<Real> gi((size_t)(si * (j - i))), gs((size_t)(3 * (j - i)));
+        const int64_t si = solid_len(p_in[idx[i]]), so = solid_len(p_out[idx[i]]);
         for (int64_t k = i; k < j; ++k) {
-            std::memcpy(&gi[(size_t)((k - i) * si)], in + in_off[idx[k]], sizeof(Real) * si);
-            std::memcpy(&gs[(size_t)(3 * (k - i))], shifts + 3 * idx[k], sizeof(Real) * 3);
+            in_pos[(size_t)k] = in_len + (k - i) * si;
+            out_pos[(size_t)k] = out_len + (k - i) * so;
         }
-        stage_in.push_back(std::move(gi));
-        stage_sh.push_back(std::move(gs));
+        in_len += si * (j - i);
+        out_len += so * (j - i);
+        max_group = std::max(max_group, j - i);
+        max_si = std::max(max_si, si * round_up32(j - i));
+        max_so = std::max(max_so, so * round_up32(j - i));
         ranges.emplace_back(i, j);
         i = j;
     }
-    for (size_t g = 0; g < ranges.size(); ++g) {
-        const int64_t i = ranges[g].first, j = ranges[g].second;
-        const int pi = p_in[idx[i]], po = p_out[idx[i]];
-        const int64_t so = solid_len(po);
-        std::vector<Real> go((size_t)(so * (j - i)));
-        const sfmm_status st = translate_host_impl<Real>(h, kind, j - i, pi, po, stage_in[g].data(),
-                                                         stage_sh[g].data(), go.data());
-        if (st != SFMM_OK) return st;
-        for (int64_t k = i; k < j; ++k)
-            std::memcpy(out + out_off[idx[k]], &go[(size_t)((k - i) * so)], sizeof(Real) * so);
+    std::vector<Real> stage_in((size_t)in_len), stage_sh((size_t)(3 * n)), stage_out((size_t)out_len);
+    for (int64_t k = 0; k < n; ++k) {
+        std::memcpy(&stage_in[(size_t)in_pos[(size_t)k]], in + in_off[idx[k]],
+                    sizeof(Real) * solid_len(p_in[idx[k]]));
+        std::memcpy(&stage_sh[(size_t)(3 * k)], shifts + 3 * idx[k], sizeof(Real) * 3);
     }
+    cudaStream_t stream = host_stream(h->device);
+    const size_t es = sizeof(Real);
+    DevBuf d_in_all(stream), d_sh_all(stream), d_out_all(stream), d_in(stream), d_out(stream);
+    CU(d_in_all.alloc(es * in_len));
+    CU(d_sh_all.alloc(es * 3 * n));
+    CU(d_out_all.alloc(es * out_len));
+    CU(d_in.alloc(es * max_si));
+    CU(d_out.alloc(es * max_so));
+    CU(cudaMemcpyAsync(d_in_all.p, stage_in.data(), es * in_len, cudaMemcpyHostToDevice, stream));
+    CU(cudaMemcpyAsync(d_sh_all.p, stage_sh.data(), es * 3 * n, cudaMemcpyHostToDevice, stream));
+    for (const auto& r : ranges) {
+        const int64_t i = r.first, m = r.second - r.first, stride = round_up32(m);
+        const int pi = p_in[idx[i]], po = p_out[idx[i]];
+        const Real* src = d_in_all.as<Real>() + in_pos[(size_t)i];
+        Real* dst = d_out_all.as<Real>() + out_pos[(size_t)i];
+        CU(launch_pack_soa<Real>(src, d_in.as<Real>(), m, pi, stride, stream));
+        const sfmm_status st =
+            translate_soa_impl<Real>(h, kind, m, pi, po, d_in.as<Real>(), stride,
+                                     d_sh_all.as<Real>() + 3 * i, d_out.as<Real>(), stride, stream, 0,
+                                     /*skip_scan=*/true);
+        if (st != SFMM_OK) return st;
+        CU(launch_unpack_soa<Real>(d_out.as<Real>(), dst, m, po, stride, stream));
+        h->launches += 2;
+    }
+    CU(cudaMemcpyAsync(stage_out.data(), d_out_all.p, es * out_len, cudaMemcpyDeviceToHost, stream));
+    CU(cudaStreamSynchronize(stream));
+    for (int64_t k = 0; k < n; ++k)
+        std::memcpy(out + out_off[idx[k]], &stage_out[(size_t)out_pos[(size_t)k]],
+                    sizeof(Real) * solid_len(p_out[idx[k]]));
     return SFMM_OK;
 }
 
@@ -327,48 +425,43 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
     plan->n_sources = n_sources;
     // the raw pair list goes to the device as it is; padding to whole groups and the
     // validation (source range, zero shifts) happen there
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = host_stream(h->device);
     const size_t padded = (size_t)std::max<int64_t>(n_groups, 1) * kPlanGroup;
     // stream-ordered allocations from the device pool (kept warm by sfmm_create): a plan
-    // per call costs no cudaMalloc / cudaFree round trips
+    // per call costs no cudaMalloc / cudaFree round trips. The plan's own buffers are freed
+    // by sfmm_plan_destroy (also on the failure paths: the caller destroys the plan).
     CU(cudaMallocAsync((void**)&plan->d_grp_ptr, sizeof(int64_t) * grp_ptr.size(), stream));
     CU(cudaMallocAsync((void**)&plan->d_src_index, sizeof(int32_t) * padded, stream));
     CU(cudaMallocAsync(&plan->d_shifts, sizeof(Real) * padded * 3, stream));
     CU(cudaMallocAsync(&plan->d_angles, sizeof(Real) * padded * 6, stream));
-    int64_t* d_tgt = nullptr;
-    int32_t *d_gt = nullptr, *d_idx = nullptr;
-    Real* d_sh = nullptr;
-    int* d_flags = nullptr;
+    plan->last_stream = stream;
+    DevBuf d_tgt(stream), d_gt(stream), d_idx(stream), d_sh(stream), d_flags(stream);
     const size_t np = (size_t)std::max<int64_t>(n_pairs, 1);
-    CU(cudaMallocAsync((void**)&d_tgt, sizeof(int64_t) * (n_targets + 1), stream));
-    CU(cudaMallocAsync((void**)&d_gt, sizeof(int32_t) * grp_target.size(), stream));
-    CU(cudaMallocAsync((void**)&d_idx, sizeof(int32_t) * np, stream));
-    CU(cudaMallocAsync((void**)&d_sh, sizeof(Real) * np * 3, stream));
-    CU(cudaMallocAsync((void**)&d_flags, sizeof(int) * 2, stream));
-    CU(cudaMemsetAsync(d_flags, 0, sizeof(int) * 2, stream));
+    CU(d_tgt.alloc(sizeof(int64_t) * (n_targets + 1)));
+    CU(d_gt.alloc(sizeof(int32_t) * grp_target.size()));
+    CU(d_idx.alloc(sizeof(int32_t) * np));
+    CU(d_sh.alloc(sizeof(Real) * np * 3));
+    CU(d_flags.alloc(sizeof(int) * 2));
+    CU(cudaMemsetAsync(d_flags.p, 0, sizeof(int) * 2, stream));
     CU(cudaMemcpyAsync(plan->d_grp_ptr, grp_ptr.data(), sizeof(int64_t) * grp_ptr.size(),
                        cudaMemcpyHostToDevice, stream));
-    CU(cudaMemcpyAsync(d_tgt, tgt_ptr, sizeof(int64_t) * (n_targets + 1), cudaMemcpyHostToDevice,
+    CU(cudaMemcpyAsync(d_tgt.p, tgt_ptr, sizeof(int64_t) * (n_targets + 1), cudaMemcpyHostToDevice,
                        stream));
-    CU(cudaMemcpyAsync(d_gt, grp_target.data(), sizeof(int32_t) * grp_target.size(),
+    CU(cudaMemcpyAsync(d_gt.p, grp_target.data(), sizeof(int32_t) * grp_target.size(),
                        cudaMemcpyHostToDevice, stream));
     if (n_pairs > 0) {
-        CU(cudaMemcpyAsync(d_idx, src_index, sizeof(int32_t) * n_pairs, cudaMemcpyHostToDevice,
+        CU(cudaMemcpyAsync(d_idx.p, src_index, sizeof(int32_t) * n_pairs, cudaMemcpyHostToDevice,
                            stream));
-        CU(cudaMemcpyAsync(d_sh, shifts, sizeof(Real) * n_pairs * 3, cudaMemcpyHostToDevice,
+        CU(cudaMemcpyAsync(d_sh.p, shifts, sizeof(Real) * n_pairs * 3, cudaMemcpyHostToDevice,
                            stream));
     }
-    CU(launch_build_plan<Real>(d_tgt, plan->d_grp_ptr, d_gt, d_idx, d_sh, n_groups, n_sources,
-                               kPlanGroup, plan->d_src_index, static_cast<Real*>(plan->d_shifts),
-                               static_cast<Real*>(plan->d_angles), d_flags, stream));
+    CU(launch_build_plan<Real>(d_tgt.as<int64_t>(), plan->d_grp_ptr, d_gt.as<int32_t>(),
+                               d_idx.as<int32_t>(), d_sh.as<Real>(), n_groups, n_sources, kPlanGroup,
+                               plan->d_src_index, static_cast<Real*>(plan->d_shifts),
+                               static_cast<Real*>(plan->d_angles), d_flags.as<int>(), stream));
     h->launches += 1;
     int flags[2] = {0, 0};
-    CU(cudaMemcpyAsync(flags, d_flags, sizeof(flags), cudaMemcpyDeviceToHost, stream));
-    cudaFreeAsync(d_tgt, stream);
-    cudaFreeAsync(d_gt, stream);
-    cudaFreeAsync(d_idx, stream);
-    cudaFreeAsync(d_sh, stream);
-    cudaFreeAsync(d_flags, stream);
+    CU(cudaMemcpyAsync(flags, d_flags.p, sizeof(flags), cudaMemcpyDeviceToHost, stream));
     CU(cudaStreamSynchronize(stream));
     if (flags[0]) return fail(SFMM_INVALID_ARGUMENT, "source index out of range");
     if (flags[1]) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
@@ -388,15 +481,16 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     // the kernel reduces the lanes of one of ITS groups (32 or 64 pairs) into one partial
     const int per = kPlanGroup / translate_group_size<Real>(tables_of<Real>(h), a);
     const int64_t n_partial = plan->n_groups * per;
-    Real* partial = nullptr;
-    if (n_partial > 0) CU(cudaMallocAsync((void**)&partial, sizeof(Real) * so * n_partial, stream));
+    DevBuf partial(stream);
+    if (n_partial > 0) CU(partial.alloc(sizeof(Real) * so * n_partial));
+    const_cast<sfmm_plan*>(plan)->last_stream = stream;
     a.n = plan->n_groups * kPlanGroup;
     a.in = d_src;
     a.in_stride = src_stride;
     a.in_layout = src_layout;
     a.shifts = static_cast<const Real*>(plan->d_shifts);
     a.angles = static_cast<const Real*>(plan->d_angles);
-    a.out = partial;
+    a.out = partial.as<Real>();
     a.out_stride = n_partial;
     a.src_index = plan->d_src_index;
     a.variant = h->variant;
@@ -405,11 +499,10 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     cudaError_t e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
     h->launches += info.launches;
     if (e == cudaSuccess) {
-        e = launch_reduce_groups<Real>(partial, n_partial, plan->d_grp_ptr, per, plan->n_targets,
-                                       p_out, d_out, out_stride, stream);
+        e = launch_reduce_groups<Real>(partial.as<Real>(), n_partial, plan->d_grp_ptr, per,
+                                       plan->n_targets, p_out, d_out, out_stride, stream);
         h->launches += 1;
     }
-    if (partial) cudaFreeAsync(partial, stream);
     if (e != cudaSuccess) return cuda_fail(e, "m2l_accumulate");
     return SFMM_OK;
 }
@@ -420,30 +513,23 @@ sfmm_status accumulate_host_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in
     const int64_t si = solid_len(p_in), so = solid_len(p_out);
     const int64_t ns = plan->n_sources, nt = plan->n_targets;
     const int64_t srows = rows_off(p_in), ostride = round_up32(nt);
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = host_stream(h->device);
     const size_t es = sizeof(Real);
-    Real *d_src_aos = nullptr, *d_src = nullptr, *d_out = nullptr, *d_out_aos = nullptr;
-    CU(cudaMallocAsync((void**)&d_src_aos, es * si * ns, stream));
-    CU(cudaMallocAsync((void**)&d_src, es * srows * ns, stream));
-    CU(cudaMallocAsync((void**)&d_out, es * so * ostride, stream));
-    CU(cudaMallocAsync((void**)&d_out_aos, es * so * nt, stream));
-    CU(cudaMemcpyAsync(d_src_aos, src_aos, es * si * ns, cudaMemcpyHostToDevice, stream));
-    CU(launch_pack_rows<Real>(d_src_aos, d_src, ns, p_in, stream));
-    sfmm_status st = accumulate_impl<Real>(h, plan, p_in, p_out, d_src, srows, LAYOUT_ROWS, d_out,
-                                           ostride, stream);
-    if (st == SFMM_OK) {
-        cudaError_t e = launch_unpack_soa<Real>(d_out, d_out_aos, nt, p_out, ostride, stream);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(out_aos, d_out_aos, es * so * nt, cudaMemcpyDeviceToHost, stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) st = cuda_fail(e, "m2l_accumulate_host");
-        h->launches += 2;
-    }
-    cudaFreeAsync(d_src_aos, stream);
-    cudaFreeAsync(d_src, stream);
-    cudaFreeAsync(d_out, stream);
-    cudaFreeAsync(d_out_aos, stream);
-    return st;
+    DevBuf d_src_aos(stream), d_src(stream), d_out(stream), d_out_aos(stream);
+    CU(d_src_aos.alloc(es * si * ns));
+    CU(d_src.alloc(es * srows * ns));
+    CU(d_out.alloc(es * so * ostride));
+    CU(d_out_aos.alloc(es * so * nt));
+    CU(cudaMemcpyAsync(d_src_aos.p, src_aos, es * si * ns, cudaMemcpyHostToDevice, stream));
+    CU(launch_pack_rows<Real>(d_src_aos.as<Real>(), d_src.as<Real>(), ns, p_in, stream));
+    const sfmm_status st = accumulate_impl<Real>(h, plan, p_in, p_out, d_src.as<Real>(), srows,
+                                                 LAYOUT_ROWS, d_out.as<Real>(), ostride, stream);
+    if (st != SFMM_OK) return st;
+    CU(launch_unpack_soa<Real>(d_out.as<Real>(), d_out_aos.as<Real>(), nt, p_out, ostride, stream));
+    CU(cudaMemcpyAsync(out_aos, d_out_aos.p, es * so * nt, cudaMemcpyDeviceToHost, stream));
+    CU(cudaStreamSynchronize(stream));
+    h->launches += 3;
+    return SFMM_OK;
 }
 
 }  // namespace
@@ -518,6 +604,7 @@ sfmm_status sfmm_create(sfmm_precision precision, int order, int device, int mu,
             cudaMemset(h->d_flags, 0, sizeof(int) * kFlagSlots) != cudaSuccess ||
             cudaMallocHost((void**)&h->h_flags, sizeof(int) * kFlagSlots) != cudaSuccess)
             st = fail(SFMM_CUDA_ERROR, "status flag allocation failed");
+        for (int i = kFlagSlots - 1; i >= 0; --i) h->free_slots.push_back(i);
     }
     if (st != SFMM_OK) {
         sfmm_destroy(h);
@@ -694,16 +781,30 @@ sfmm_status sfmm_stream_status(sfmm_handle* h, void* stream) {
     if (!h) return fail(SFMM_INVALID_ARGUMENT, "null handle");
     DeviceGuard guard(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // only the calls issued on this stream: the others have not necessarily run yet and
+    // keep their slots until their own stream is queried
     std::vector<int> slots;
     {
         std::lock_guard<std::mutex> lk(h->async_mutex);
-        slots.swap(h->async_slots);
+        auto keep = h->pending.begin();
+        for (auto it = h->pending.begin(); it != h->pending.end(); ++it) {
+            if (it->stream == s) slots.push_back(it->slot);
+            else *keep++ = *it;
+        }
+        h->pending.erase(keep, h->pending.end());
     }
-    CU(cudaMemcpyAsync(h->h_flags, h->d_flags, sizeof(int) * kFlagSlots, cudaMemcpyDeviceToHost,
-                       s));
-    CU(cudaStreamSynchronize(s));
-    for (int slot : slots)
-        if (h->h_flags[slot]) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
+    std::vector<int> values(kFlagSlots, 0);
+    cudaError_t e = cudaSuccess;
+    if (!slots.empty())
+        e = cudaMemcpyAsync(values.data(), h->d_flags, sizeof(int) * kFlagSlots, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    bool bad = false;
+    for (int slot : slots) {
+        bad = bad || values[slot] != 0;
+        release_slot(h, slot);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "sfmm_stream_status");
+    if (bad) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
     return SFMM_OK;
 }
 
@@ -781,11 +882,13 @@ void sfmm_plan_destroy(sfmm_plan* plan) {
     if (!plan) return;
     if (plan->h) {
         DeviceGuard guard(plan->h->device);
-        // ordered on the legacy default stream: behind all work of blocking streams
-        cudaFreeAsync(plan->d_grp_ptr, nullptr);
-        cudaFreeAsync(plan->d_src_index, nullptr);
-        cudaFreeAsync(plan->d_shifts, nullptr);
-        cudaFreeAsync(plan->d_angles, nullptr);
+        // ordered behind the most recent accumulate call that used the plan (calls on several
+        // streams at once: synchronise the others before destroying, solidfmm_b200.h)
+        cudaStream_t s = plan->last_stream;
+        if (plan->d_grp_ptr) cudaFreeAsync(plan->d_grp_ptr, s);
+        if (plan->d_src_index) cudaFreeAsync(plan->d_src_index, s);
+        if (plan->d_shifts) cudaFreeAsync(plan->d_shifts, s);
+        if (plan->d_angles) cudaFreeAsync(plan->d_angles, s);
     }
     delete plan;
 }

@@ -153,16 +153,12 @@ __global__ void dmma_peak_kernel(double* out, int iters, double a, double b) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
-int g_smem_optin = -1;
-
+// opt-in shared memory of the CURRENT device (handles live on any device)
 int smem_optin_limit() {
-    if (g_smem_optin < 0) {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        g_smem_optin = v;
-    }
-    return g_smem_optin;
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
 }
 
 }  // namespace

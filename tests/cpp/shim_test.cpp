@@ -223,6 +223,13 @@ int main() {
         std::vector<translation_request<double>> reqs{{&m, {1, 0, 0}, 6, &o1}, {&m, {0, 0, 0}, 6, &o2}};
         CHECK(throws<std::domain_error>([&] { m2l<double>(ops, reqs, ws); }));
         CHECK(o1.re(0, 0) == 42.0);
+        // validation is per request, in order (pipeline.cpp:282-298): the zero shift of request
+        // 0 is reported, not the bad order of request 1 ... and the other way round
+        std::vector<translation_request<double>> mixed{{&m, {0, 0, 0}, 6, &o1}, {&m, {1, 0, 0}, 7, &o2}};
+        CHECK(throws<std::domain_error>([&] { m2l<double>(ops, mixed, ws); }));
+        std::vector<translation_request<double>> mixed2{{&m, {1, 0, 0}, 7, &o1}, {&m, {0, 0, 0}, 6, &o2}};
+        CHECK(throws<std::invalid_argument>([&] { m2l<double>(ops, mixed2, ws); }));
+        CHECK(o1.re(0, 0) == 42.0);
     }
     // single precision (:320-335)
     {

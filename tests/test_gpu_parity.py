@@ -405,3 +405,60 @@ def test_handle_tables_and_device_soa_path(oracle, h64):
         h64.stream_status(stream)
     assert torch.all(d_out == 5.0)
     assert h64.launch_count > 0
+
+
+def test_async_status_is_per_stream_and_never_lost(oracle, h64):
+    """SFMM_ASYNC_STATUS bookkeeping: a failure stays with the stream it was issued on until
+    that stream is queried; more unqueried calls than flag slots do not overwrite it."""
+    import torch
+    rng = np.random.default_rng(211)
+    n, p = 200, 6
+    x, sh = random_solids(rng, n, p), random_shifts(rng, n)
+    bad = sh.copy()
+    bad[5] = 0.0
+    dev = torch.device("cuda", 0)
+    S, stride = solid_size(p), 256
+    d_aos = torch.from_numpy(x).to(dev)
+    d_in = torch.zeros((S, stride), dtype=torch.float64, device=dev)
+    h64.pack_soa(n, p, d_aos.data_ptr(), d_in.data_ptr(), stride)
+    d_good, d_bad = torch.from_numpy(sh).to(dev), torch.from_numpy(bad).to(dev)
+    d_out_a = torch.full((S, stride), 9.0, dtype=torch.float64, device=dev)
+    d_out_b = torch.full((S, stride), 9.0, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    args = (capi.M2L, n, p, p, d_in.data_ptr(), stride)
+    h64.translate_soa(*args, d_bad.data_ptr(), d_out_a.data_ptr(), stride, sa.cuda_stream, capi.ASYNC_STATUS)
+    h64.translate_soa(*args, d_good.data_ptr(), d_out_b.data_ptr(), stride, sb.cuda_stream, capi.ASYNC_STATUS)
+    h64.stream_status(sb.cuda_stream)                       # the other stream's failure is not consumed
+    with pytest.raises(capi.DomainError):
+        h64.stream_status(sa.cuda_stream)
+    h64.stream_status(sa.cuda_stream)                       # reported once
+    assert torch.all(d_out_a == 9.0) and not torch.any(d_out_b[:, :n] == 9.0)
+    # a failure followed by more unqueried calls than there are flag slots
+    h64.translate_soa(*args, d_bad.data_ptr(), d_out_a.data_ptr(), stride, sa.cuda_stream, capi.ASYNC_STATUS)
+    for _ in range(300):
+        h64.translate_soa(*args, d_good.data_ptr(), d_out_b.data_ptr(), stride, sa.cuda_stream, capi.ASYNC_STATUS)
+    with pytest.raises(capi.DomainError):
+        h64.stream_status(sa.cuda_stream)
+    h64.stream_status(sa.cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.all(d_out_a == 9.0)
+
+
+def test_binding_rejects_bad_host_buffers(h64):
+    rng = np.random.default_rng(223)
+    m, sh = random_solids(rng, 3, 6), random_shifts(rng, 3, with_axes=False)
+    with pytest.raises(capi.InvalidArgument):
+        h64.translate_host(capi.M2L, 6, 6, m, sh, np.empty((3, solid_size(6)), np.float32))
+    with pytest.raises(capi.InvalidArgument):
+        h64.translate_host(capi.M2L, 6, 6, m, sh, np.empty((2, solid_size(6))))
+    with pytest.raises(capi.InvalidArgument):
+        h64.translate_host(capi.M2L, 6, 6, m[:2], sh)
+    with pytest.raises(capi.InvalidArgument):
+        h64.translate_host(capi.M2L, 6, 6, m, sh, np.empty((solid_size(6), 6)).T[:3])
+    plan = h64.plan([0, 2], [0, 1], sh[:2], 2)
+    with pytest.raises(capi.InvalidArgument):
+        plan.accumulate_host(6, 6, m[:1])
+    with pytest.raises(capi.InvalidArgument):
+        plan.accumulate_host(6, 6, m[:2], np.empty((1, solid_size(6)), np.float32))
+    plan.close()
