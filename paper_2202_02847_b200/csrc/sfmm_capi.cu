@@ -478,7 +478,11 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.p_in = p_in;
     a.p_out = p_out;
     a.variant = h->variant;
-    // the kernel reduces the lanes of one of ITS groups (32 or 64 pairs) into one partial
+    a.src_index = plan->d_src_index;  // accumulate mode decides which kernels apply
+    a.in_layout = src_layout;
+    if (translate_variant<Real>(tables_of<Real>(h), a) == 0)
+        return fail(SFMM_INVALID_ARGUMENT, "the selected kernel variant does not apply to this call");
+    // the kernel reduces the lanes of one of ITS groups (16, 32 or 64 pairs) into one partial
     const int per = kPlanGroup / translate_group_size<Real>(tables_of<Real>(h), a);
     const int64_t n_partial = plan->n_groups * per;
     DevBuf partial(stream);
@@ -630,10 +634,12 @@ int sfmm_accumulation_unit(const sfmm_handle* h, int p_in, int p_out) {
     if (h->precision == SFMM_F64) {
         TranslateArgs<double> a;
         a.kind = KIND_M2L, a.p_in = p_in, a.p_out = p_out, a.variant = h->variant;
+        a.src_index = h->d_flags;  // any non-null pointer: accumulate mode (never dereferenced)
         return translate_group_size<double>(h->td, a);
     }
     TranslateArgs<float> a;
     a.kind = KIND_M2L, a.p_in = p_in, a.p_out = p_out, a.variant = h->variant;
+    a.src_index = h->d_flags;
     return translate_group_size<float>(h->tf, a);
 }
 
