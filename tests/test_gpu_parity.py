@@ -462,3 +462,16 @@ def test_binding_rejects_bad_host_buffers(h64):
     with pytest.raises(capi.InvalidArgument):
         plan.accumulate_host(6, 6, m[:2], np.empty((1, solid_size(6)), np.float32))
     plan.close()
+
+
+def test_accuracy_dominance_p20(oracle, ref, h64):
+    """SURVEY 7.1 / acceptance.cpp:87-118: at P = 20 the fast algorithm sits ~5e-12 from the
+    O(P^4) kernel whoever runs it. The GPU result must be at least as close to the naive
+    kernel as the reference's own m2l (it is the same numbers, so: exactly as close)."""
+    src, sh = workloads.config0(60, 128, 20)
+    gpu = run(h64, "m2l", 20, 20, src, sh)
+    _, naive = oracle.m2l_naive(20, 20, src, sh)
+    _, r = ref.translate("m2l", 20, 20, src, sh)
+    e_gpu, e_ref = normalized_error(gpu, naive), normalized_error(r, naive)
+    assert e_gpu <= e_ref and e_gpu < 1e-10
+    assert bits_equal(gpu, r)
