@@ -1,7 +1,7 @@
 """DRAM traffic of the dominant kernel of a bench case from an `ncu --set full` report.
 
-usage: ncu_traffic.py <report.ncu-rep> <config:case> [kernel-regex]
-Reads `ncu -i <report> --page raw --csv`, takes the launches whose name matches the regex
+usage: ncu_traffic.py <report.ncu-rep | raw-page.csv> <config:case> [kernel-regex]
+Reads `ncu -i <report> --page raw --csv` (or that page already exported to a file), takes the launches whose name matches the regex
 (default: translate), averages dram__bytes_read.sum + dram__bytes_write.sum over them and
 records the result in profiles/ncu_traffic_r02.json, which bench.py quotes as
 `roofline.traffic` (never a literal in the source)."""
@@ -16,8 +16,11 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 rep, key = sys.argv[1], sys.argv[2]
 pattern = re.compile(sys.argv[3] if len(sys.argv) > 3 else "translate")
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], stdout=subprocess.PIPE, text=True,
-                     check=True).stdout
+if rep.endswith(".csv"):
+    raw = Path(rep).read_text()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], stdout=subprocess.PIPE, text=True,
+                         check=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 ix = {h: i for i, h in enumerate(hdr)}
