@@ -331,6 +331,27 @@ def run_reference_arm(args, case: Case, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def build_level_once(rank: int, world: int, dist):
+    """The level is generated once per node (rank 0) and shared through /dev/shm."""
+    path = Path("/dev/shm") / f"solidfmm_b200_level_{os.environ.get('MASTER_PORT', '0')}.npz"
+    if rank == 0:
+        t0 = time.time()
+        lvl = workloads.config3(0, GRID, 20)
+        log(f"[bench] level built in {time.time() - t0:.1f}s: {len(lvl[0])} sources, "
+            f"{len(lvl[1]) - 1} targets, {len(lvl[2])} pairs")
+        if world > 1:
+            np.savez(path, sources=lvl[0], tgt_ptr=lvl[1], src_index=lvl[2], shifts=lvl[3])
+    if world > 1:
+        dist.barrier()
+        if rank != 0:
+            z = np.load(path)
+            lvl = (z["sources"], z["tgt_ptr"], z["src_index"], z["shifts"])
+        dist.barrier()
+        if rank == 0:
+            path.unlink(missing_ok=True)
+    return lvl
+
+
 # ---------------------------------------------------------------------------
 
 def main():
@@ -384,13 +405,14 @@ def main():
         return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
 
     if case.level:
-        t0 = time.time()
-        sources, tgt_ptr, src_index, shifts = workloads.config3(0, GRID, 20)
-        log(f"[bench] level built in {time.time() - t0:.1f}s: {len(sources)} sources, "
-            f"{len(tgt_ptr) - 1} targets, {len(src_index)} pairs")
+        sources, tgt_ptr, src_index, shifts = build_level_once(rank, world, dist if world > 1 else None)
         t_lo, t_hi, my_ptr, my_idx, my_shifts = sharding.shard_plan(tgt_ptr, src_index, shifts, rank, world)
         my_units, total_units = len(my_idx), int(tgt_ptr[-1])
         my_targets = t_hi - t_lo
+        if world > 1:
+            # a rank holds and uploads only the sources its targets reference (halo slab)
+            used, my_idx = sharding.compact_sources(my_idx)
+            sources = np.ascontiguousarray(sources[used])
         n_src = len(sources)
         # resident inputs of the device-timed `value`: sources in the library's rows layout
         # (include/solidfmm_b200.h: sfmm_pack_rows), outputs SoA

@@ -48,13 +48,14 @@ struct DeviceGuard {
 // Stream of the host-buffer entry points: one non-blocking stream per calling thread and
 // device, so that concurrent callers (one workspace per thread in the reference,
 // pipeline.hpp:30-45) neither serialise on the legacy default stream nor on each other.
-cudaStream_t host_stream(int device) {
+cudaStream_t host_stream(int device, int which = 0) {
     thread_local std::vector<std::pair<int, cudaStream_t>> cache;
+    const int key = device * 2 + which;
     for (const auto& e : cache)
-        if (e.first == device) return e.second;
+        if (e.first == key) return e.second;
     cudaStream_t s = nullptr;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) s = nullptr;
-    cache.emplace_back(device, s);
+    cache.emplace_back(key, s);
     return s;
 }
 
@@ -296,31 +297,58 @@ sfmm_status translate_host_impl(sfmm_handle* h, int kind, int64_t n, int p_in, i
         if (host_shift_degenerate(shifts + 3 * i))
             return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
     const int64_t si = solid_len(p_in), so = solid_len(p_out);
-    // staged in chunks: the device scratch stays bounded however large the batch is, and
-    // everything is ordered on one stream with a single synchronisation at the end
-    const int64_t chunk = std::min(n, kHostChunk), stride = round_up32(chunk);
-    cudaStream_t stream = host_stream(h->device);
-    DevBuf d_in_aos(stream), d_in(stream), d_sh(stream), d_out(stream), d_out_aos(stream);
+    // Staged in chunks on two streams: the device scratch stays bounded however large the
+    // batch is, and the upload of chunk i+1 overlaps the kernels and the download of chunk i
+    // (the link is full duplex; from pinned host memory the copies are asynchronous).
+    int64_t chunk = std::min(n, kHostChunk);
+    if (n >= 8 * 32768) chunk = std::min(chunk, (n / 8 + 31) / 32 * 32);
+    const int64_t stride = round_up32(chunk);
+    const int lanes = n > chunk ? 2 : 1;
     const size_t es = sizeof(Real);
-    CU(d_in_aos.alloc(es * si * chunk));
-    CU(d_in.alloc(es * si * stride));
-    CU(d_sh.alloc(es * 3 * chunk));
-    CU(d_out.alloc(es * so * stride));
-    CU(d_out_aos.alloc(es * so * chunk));
-    for (int64_t lo = 0; lo < n; lo += chunk) {
+    struct Lane {
+        cudaStream_t stream;
+        DevBuf in_aos, in, sh, out, out_aos;
+        explicit Lane(cudaStream_t s) : stream(s), in_aos(s), in(s), sh(s), out(s), out_aos(s) {}
+    };
+    Lane lane0(host_stream(h->device, 0)), lane1(host_stream(h->device, 1));
+    Lane* lane[2] = {&lane0, &lane1};
+    for (int l = 0; l < lanes; ++l) {
+        CU(lane[l]->in_aos.alloc(es * si * chunk));
+        CU(lane[l]->in.alloc(es * si * stride));
+        CU(lane[l]->sh.alloc(es * 3 * chunk));
+        CU(lane[l]->out.alloc(es * so * stride));
+        CU(lane[l]->out_aos.alloc(es * so * chunk));
+    }
+    sfmm_status st = SFMM_OK;
+    cudaError_t e = cudaSuccess;
+    int64_t c = 0;
+    for (int64_t lo = 0; lo < n && st == SFMM_OK && e == cudaSuccess; lo += chunk, ++c) {
+        Lane& L = *lane[c & (lanes - 1)];
         const int64_t m = std::min(chunk, n - lo);
-        CU(cudaMemcpyAsync(d_in_aos.p, in + lo * si, es * si * m, cudaMemcpyHostToDevice, stream));
-        CU(cudaMemcpyAsync(d_sh.p, shifts + 3 * lo, es * 3 * m, cudaMemcpyHostToDevice, stream));
-        CU(launch_pack_soa<Real>(d_in_aos.as<Real>(), d_in.as<Real>(), m, p_in, stride, stream));
-        const sfmm_status st =
-            translate_soa_impl<Real>(h, kind, m, p_in, p_out, d_in.as<Real>(), stride, d_sh.as<Real>(),
-                                     d_out.as<Real>(), stride, stream, 0, /*skip_scan=*/true);
-        if (st != SFMM_OK) return st;
-        CU(launch_unpack_soa<Real>(d_out.as<Real>(), d_out_aos.as<Real>(), m, p_out, stride, stream));
-        CU(cudaMemcpyAsync(out + lo * so, d_out_aos.p, es * so * m, cudaMemcpyDeviceToHost, stream));
+        e = cudaMemcpyAsync(L.in_aos.p, in + lo * si, es * si * m, cudaMemcpyHostToDevice, L.stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(L.sh.p, shifts + 3 * lo, es * 3 * m, cudaMemcpyHostToDevice, L.stream);
+        if (e == cudaSuccess)
+            e = launch_pack_soa<Real>(L.in_aos.template as<Real>(), L.in.template as<Real>(), m, p_in, stride,
+                                      L.stream);
+        if (e != cudaSuccess) break;
+        st = translate_soa_impl<Real>(h, kind, m, p_in, p_out, L.in.template as<Real>(), stride,
+                                      L.sh.template as<Real>(), L.out.template as<Real>(), stride, L.stream, 0,
+                                      /*skip_scan=*/true);
+        if (st != SFMM_OK) break;
+        e = launch_unpack_soa<Real>(L.out.template as<Real>(), L.out_aos.template as<Real>(), m, p_out, stride,
+                                    L.stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out + lo * so, L.out_aos.p, es * so * m, cudaMemcpyDeviceToHost, L.stream);
         h->launches += 2;
     }
-    CU(cudaStreamSynchronize(stream));
+    // both streams are drained on every path: the scratch is released behind them
+    for (int l = 0; l < lanes; ++l) {
+        const cudaError_t e2 = cudaStreamSynchronize(lane[l]->stream);
+        if (e == cudaSuccess) e = e2;
+    }
+    if (st != SFMM_OK) return st;
+    if (e != cudaSuccess) return cuda_fail(e, "translate_host");
     return SFMM_OK;
 }
 

@@ -32,6 +32,14 @@ def shard_plan(tgt_ptr: np.ndarray, src_index: np.ndarray, shifts: np.ndarray, r
             np.ascontiguousarray(shifts[p_lo:p_hi]))
 
 
+def compact_sources(local_src_index: np.ndarray):
+    """The sources a rank's pair list references (its halo slab) and the pair list re-indexed
+    into that compact set: a rank then holds and uploads only what its targets need instead
+    of every source of the level. Returns (used [k] ascending global indices, remapped [pairs])."""
+    used, remapped = np.unique(local_src_index, return_inverse=True)
+    return used.astype(np.int64), remapped.astype(np.int32)
+
+
 def accumulation_tree(per_pair: np.ndarray, tgt_ptr: np.ndarray, unit: int = 64) -> np.ndarray:
     """The library's fixed summation order for target-owned accumulation, restated
     in numpy; `per_pair` holds one output solid

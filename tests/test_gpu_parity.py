@@ -475,3 +475,28 @@ def test_accuracy_dominance_p20(oracle, ref, h64):
     e_gpu, e_ref = normalized_error(gpu, naive), normalized_error(r, naive)
     assert e_gpu <= e_ref and e_gpu < 1e-10
     assert bits_equal(gpu, r)
+
+
+def test_sharded_level_over_all_visible_devices(oracle, h64):
+    """One handle and one target range per visible device, halo sources only: the
+    concatenated shards equal the single-device result bit for bit (no collective on the
+    data path). Needs at least two GPUs."""
+    import torch
+    world = torch.cuda.device_count()
+    if world < 2:
+        pytest.skip("one visible device")
+    p = 12
+    src, tgt_ptr, idx, sh = workloads.config3(3, (4, 2, 2), p)
+    plan = h64.plan(tgt_ptr, idx, sh, len(src))
+    want = plan.accumulate_host(p, p, src)
+    plan.close()
+    parts = []
+    for rank in range(world):
+        t_lo, t_hi, lptr, lidx, lsh = sharding.shard_plan(tgt_ptr, idx, sh, rank, world)
+        used, lidx = sharding.compact_sources(lidx)
+        h = capi.Handle(capi.F64, p, device=rank)
+        lp = h.plan(lptr, lidx, lsh, len(used))
+        parts.append(lp.accumulate_host(p, p, src[used]))
+        lp.close()
+        h.close()
+    assert bits_equal(np.concatenate(parts), want)

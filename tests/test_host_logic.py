@@ -179,3 +179,15 @@ def test_accumulation_tree_is_a_sum():
     for t in range(5):
         assert np.allclose(got[t], per_pair[ptr[t]:ptr[t + 1]].sum(axis=0), rtol=1e-13)
     assert np.array_equal(got[0], per_pair[0])            # a single pair is copied exactly
+
+
+def test_compact_sources_is_a_relabelling():
+    """A rank's halo slab: the compact set holds exactly the referenced sources and the
+    re-indexed pair list points at the same expansions."""
+    rng = np.random.default_rng(5)
+    idx = rng.integers(0, 500, 2000).astype(np.int32)
+    used, remapped = sharding.compact_sources(idx)
+    assert np.array_equal(used, np.unique(idx)) and remapped.dtype == np.int32
+    assert np.array_equal(used[remapped], idx)
+    src = rng.standard_normal((500, 6))
+    assert np.array_equal(src[used][remapped], src[idx])
