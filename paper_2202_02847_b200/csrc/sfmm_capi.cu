@@ -241,7 +241,8 @@ sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, in
             CU(spare.alloc(sizeof(int)));
             d_flag = spare.as<int>();
         }
-        cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), stream);
+        // free slots are zero (zeroed at creation and whenever a failure has been read)
+        cudaError_t e = slot >= 0 ? cudaSuccess : cudaMemsetAsync(d_flag, 0, sizeof(int), stream);
         if (e == cudaSuccess) e = launch_check_shifts<Real>(d_shifts, n, d_flag, stream);
         if (e != cudaSuccess) {
             if (slot >= 0) release_slot(h, slot);
@@ -267,6 +268,8 @@ sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, in
     if (e != cudaSuccess) {
         if (slot >= 0) {
             cudaStreamSynchronize(stream);  // the scan may still write the slot
+            cudaMemsetAsync(d_flag, 0, sizeof(int), stream);
+            cudaStreamSynchronize(stream);
             release_slot(h, slot);
         }
         return cuda_fail(e, "launch_translate");
@@ -284,7 +287,13 @@ sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, in
     e = cudaMemcpyAsync(dst, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     const int bad = *dst;
-    if (slot >= 0) release_slot(h, slot);
+    if (slot >= 0) {
+        if (bad || e != cudaSuccess) {  // back to the free-slot invariant before the slot is reused
+            cudaMemsetAsync(d_flag, 0, sizeof(int), stream);
+            cudaStreamSynchronize(stream);
+        }
+        release_slot(h, slot);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "zero-shift status");
     if (bad) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
     return SFMM_OK;
@@ -301,7 +310,7 @@ sfmm_status translate_host_impl(sfmm_handle* h, int kind, int64_t n, int p_in, i
     // batch is, and the upload of chunk i+1 overlaps the kernels and the download of chunk i
     // (the link is full duplex; from pinned host memory the copies are asynchronous).
     int64_t chunk = std::min(n, kHostChunk);
-    if (n >= 8 * 32768) chunk = std::min(chunk, (n / 8 + 31) / 32 * 32);
+    if (n >= 65536) chunk = std::min(chunk, (n / 8 + 31) / 32 * 32);
     const int64_t stride = round_up32(chunk);
     const int lanes = n > chunk ? 2 : 1;
     const size_t es = sizeof(Real);
@@ -834,9 +843,13 @@ sfmm_status sfmm_stream_status(sfmm_handle* h, void* stream) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     bool bad = false;
     for (int slot : slots) {
-        bad = bad || values[slot] != 0;
-        release_slot(h, slot);
+        if (values[slot] != 0 || e != cudaSuccess) {
+            bad = bad || values[slot] != 0;
+            cudaMemsetAsync(h->d_flags + slot, 0, sizeof(int), s);  // free slots are zero
+        }
     }
+    if (bad || e != cudaSuccess) cudaStreamSynchronize(s);
+    for (int slot : slots) release_slot(h, slot);
     if (e != cudaSuccess) return cuda_fail(e, "sfmm_stream_status");
     if (bad) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
     return SFMM_OK;
