@@ -433,13 +433,12 @@ def main():
         out_host = torch.empty((my_targets, S_out), dtype=tdt).pin_memory().numpy()
 
         def step_e2e():
-            p = handle.plan(h_ptr, h_idx, h_shifts, n_src)
-            p.accumulate_host(20, 20, h_src, out_host)
-            p.close()
+            handle.m2l_level_host(h_ptr, h_idx, h_shifts, 20, 20, h_src, out_host)
 
         h2d = sources.nbytes + my_idx.nbytes + my_shifts.nbytes + my_ptr.nbytes
         d2h = out_host.nbytes
-        e2e_path = "sfmm_plan_create + sfmm_m2l_accumulate_host from pinned host arrays"
+        e2e_path = ("sfmm_m2l_level_host (pair list and sources from pinned host arrays -> plan -> "
+                    "kernels -> locals to the host), pipelined over 4 target slabs")
         workload_cfg = {"targets": len(tgt_ptr) - 1, "sources": n_src, "pairs": total_units,
                         "partition": f"targets/{world}"}
     else:

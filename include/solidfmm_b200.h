@@ -174,6 +174,18 @@ sfmm_status sfmm_m2l_accumulate_host(sfmm_handle* h, const sfmm_plan* plan,
                                      int p_in, int p_out, const void* src_aos,
                                      void* out_aos);
 
+/* One-shot form: plan + accumulation of one level from host arrays in a single call
+ * (arguments as sfmm_plan_create and sfmm_m2l_accumulate_host). Large levels are pipelined
+ * over slabs of targets: the pair list of the next slab uploads and the locals of the
+ * previous slab download while the current slab computes. Results are bit-identical to the
+ * two-call form; on INVALID_ARGUMENT / DOMAIN_ERROR nothing has been written to out_aos
+ * (pipeline.cpp:282-298). "level_slab_pairs" (sfmm_set_option) sets the slab size from which
+ * the pipeline is used (default 2^18 pairs per slab). */
+sfmm_status sfmm_m2l_level_host(sfmm_handle* h, int64_t n_targets, const int64_t* tgt_ptr,
+                                const int32_t* src_index, const void* shifts,
+                                int64_t n_sources, int p_in, int p_out, const void* src_aos,
+                                void* out_aos);
+
 /* Summation unit of sfmm_m2l_accumulate* for this order pair with the kernel the
  * handle would choose: 64 = pairs j and j+32 of a 64-pair group are added first,
  * then the 32 sums by the xor butterfly (lane distances 16, 8, 4, 2, 1); 32 or 16 =

@@ -54,6 +54,8 @@ _SIGNATURES = {
     "sfmm_m2l_accumulate": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_int64, c_void_p,
                                     c_int64, c_void_p]),
     "sfmm_m2l_accumulate_host": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "sfmm_m2l_level_host": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_int,
+                                    c_int, c_void_p, c_void_p]),
     "sfmm_accumulation_unit": (c_int, [c_void_p, c_int, c_int]),
     "sfmm_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
     "sfmm_measure_fma_peak": (c_int, [c_void_p, POINTER(c_double)]),
@@ -296,6 +298,24 @@ class Handle:
     # -- target-owned accumulation -----------------------------------------
     def plan(self, tgt_ptr, src_index, shifts, n_sources: int) -> "Plan":
         return Plan(self, tgt_ptr, src_index, shifts, n_sources)
+
+    def m2l_level_host(self, tgt_ptr, src_index, shifts, p_in: int, p_out: int, src: np.ndarray,
+                       out: np.ndarray | None = None) -> np.ndarray:
+        """One-shot level from host arrays (plan + accumulation, pipelined over target slabs)."""
+        tgt_ptr = np.ascontiguousarray(tgt_ptr, np.int64)
+        src_index = np.ascontiguousarray(src_index, np.int32)
+        shifts = np.ascontiguousarray(shifts, self.dtype)
+        src = np.ascontiguousarray(src, self.dtype)
+        n_targets = len(tgt_ptr) - 1
+        n_sources = src.size // solid_size(p_in)
+        if out is None:
+            out = np.empty((n_targets, solid_size(p_out)), self.dtype)
+        _check_buffer(out, self.dtype, n_targets * solid_size(p_out), "out")
+        if len(src_index) < tgt_ptr[-1] or shifts.size < 3 * tgt_ptr[-1]:
+            raise InvalidArgument(INVALID_ARGUMENT, "pair arrays shorter than tgt_ptr[-1]")
+        check(self._lib.sfmm_m2l_level_host(self._h, n_targets, _ptr(tgt_ptr), _ptr(src_index),
+                                            _ptr(shifts), n_sources, p_in, p_out, _ptr(src), _ptr(out)))
+        return out
 
 
 class Plan:

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -107,6 +108,7 @@ struct sfmm_handle {
     std::vector<int> free_slots;
     std::vector<Pending> pending;
     int variant = 0;
+    int64_t level_slab_pairs = 1 << 18;   // sfmm_m2l_level_host pipelines from 4 x this many pairs
     long long* d_phase_clocks = nullptr;  // set by the "phase_clocks" option
 };
 
@@ -573,6 +575,158 @@ sfmm_status accumulate_host_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in
     return SFMM_OK;
 }
 
+// One-shot level (plan + accumulation) from host arrays, pipelined over target slabs:
+// the pair list of slab k+1 uploads while slab k computes, the locals of slab k download
+// while slab k+1 computes. Nothing is written to `out_aos` before every slab has passed the
+// validation (pipeline.cpp:282-298: all requests are checked before any output is touched).
+template <typename Real>
+sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tgt_ptr,
+                            const int32_t* src_index, const Real* shifts, int64_t n_sources, int p_in,
+                            int p_out, const Real* src_aos, Real* out_aos) {
+    const int64_t n_pairs = tgt_ptr[n_targets];
+    const int K = n_pairs >= 4 * h->level_slab_pairs ? 4 : (n_pairs >= 2 * h->level_slab_pairs ? 2 : 1);
+    if (K == 1) {
+        sfmm_plan plan;
+        sfmm_status st = plan_create_impl<Real>(h, n_targets, tgt_ptr, src_index, shifts, n_sources, &plan);
+        if (st == SFMM_OK) st = accumulate_host_impl<Real>(h, &plan, p_in, p_out, src_aos, out_aos);
+        cudaStream_t s = plan.last_stream;
+        if (plan.d_grp_ptr) cudaFreeAsync(plan.d_grp_ptr, s);
+        if (plan.d_src_index) cudaFreeAsync(plan.d_src_index, s);
+        if (plan.d_shifts) cudaFreeAsync(plan.d_shifts, s);
+        if (plan.d_angles) cudaFreeAsync(plan.d_angles, s);
+        return st;
+    }
+    for (int64_t t = 0; t < n_targets; ++t)
+        if (tgt_ptr[t + 1] < tgt_ptr[t]) return fail(SFMM_INVALID_ARGUMENT, "tgt_ptr must be non-decreasing");
+    const int64_t si = solid_len(p_in), so = solid_len(p_out), srows = rows_off(p_in);
+    const size_t es = sizeof(Real);
+    cudaStream_t sc = host_stream(h->device, 0), sx = host_stream(h->device, 1);
+    // slabs of about equal pair counts, cut at target boundaries
+    std::vector<int64_t> cut(K + 1, n_targets);
+    cut[0] = 0;
+    for (int k = 1; k < K; ++k)
+        cut[k] = std::lower_bound(tgt_ptr, tgt_ptr + n_targets + 1, n_pairs * k / K) - tgt_ptr;
+    struct Slab {
+        sfmm_plan plan;
+        std::vector<int64_t> grp_ptr;
+        std::vector<int32_t> grp_target;
+        DevBuf tgt, gt, idx, sh, out, out_aos;
+        cudaEvent_t ready = nullptr, done = nullptr;
+        int64_t t0 = 0, ostride = 0;
+        explicit Slab(cudaStream_t c, cudaStream_t x) : tgt(c), gt(c), idx(c), sh(c), out(x), out_aos(x) {}
+    };
+    // declared before the guard below: the guard drains the streams first, then the buffers go
+    DevBuf d_src_aos(sc), d_src(sc), d_flags(sc);
+    std::vector<std::unique_ptr<Slab>> slabs;
+    cudaEvent_t ev_src = nullptr;
+    struct Drain {
+        cudaStream_t a, b;
+        std::vector<std::unique_ptr<Slab>>* slabs;
+        cudaEvent_t* ev;
+        ~Drain() {
+            cudaStreamSynchronize(a);
+            cudaStreamSynchronize(b);
+            for (auto& s : *slabs) {
+                if (s->ready) cudaEventDestroy(s->ready);
+                if (s->done) cudaEventDestroy(s->done);
+                sfmm_plan& p = s->plan;
+                if (p.d_grp_ptr) cudaFreeAsync(p.d_grp_ptr, a);
+                if (p.d_src_index) cudaFreeAsync(p.d_src_index, a);
+                if (p.d_shifts) cudaFreeAsync(p.d_shifts, a);
+                if (p.d_angles) cudaFreeAsync(p.d_angles, a);
+            }
+            if (*ev) cudaEventDestroy(*ev);
+        }
+    } drain{sc, sx, &slabs, &ev_src};
+
+    CU(cudaEventCreateWithFlags(&ev_src, cudaEventDisableTiming));
+    CU(d_src_aos.alloc(es * si * n_sources));
+    CU(d_src.alloc(es * srows * n_sources));
+    CU(d_flags.alloc(sizeof(int) * 2 * K));
+    CU(cudaMemsetAsync(d_flags.p, 0, sizeof(int) * 2 * K, sc));
+    CU(cudaMemcpyAsync(d_src_aos.p, src_aos, es * si * n_sources, cudaMemcpyHostToDevice, sc));
+    CU(launch_pack_rows<Real>(d_src_aos.as<Real>(), d_src.as<Real>(), n_sources, p_in, sc));
+    CU(cudaEventRecord(ev_src, sc));
+    CU(cudaStreamWaitEvent(sx, ev_src, 0));
+    h->launches += 1;
+    for (int k = 0; k < K; ++k) {
+        slabs.emplace_back(new Slab(sc, sx));
+        Slab& S = *slabs.back();
+        const int64_t t0 = cut[k], t1 = cut[k + 1], nt = t1 - t0;
+        const int64_t p0 = tgt_ptr[t0], np = tgt_ptr[t1] - p0;
+        S.t0 = t0;
+        S.ostride = round_up32(std::max<int64_t>(nt, 1));
+        S.grp_ptr.assign((size_t)nt + 1, 0);
+        for (int64_t t = 0; t < nt; ++t)
+            S.grp_ptr[(size_t)t + 1] =
+                S.grp_ptr[(size_t)t] + (tgt_ptr[t0 + t + 1] - tgt_ptr[t0 + t] + kPlanGroup - 1) / kPlanGroup;
+        const int64_t n_groups = S.grp_ptr[(size_t)nt];
+        S.grp_target.resize((size_t)std::max<int64_t>(n_groups, 1));
+        for (int64_t t = 0; t < nt; ++t)
+            for (int64_t g = S.grp_ptr[(size_t)t]; g < S.grp_ptr[(size_t)t + 1]; ++g)
+                S.grp_target[(size_t)g] = (int32_t)t;
+        std::vector<int64_t> local_ptr((size_t)nt + 1);
+        for (int64_t t = 0; t <= nt; ++t) local_ptr[(size_t)t] = tgt_ptr[t0 + t] - p0;
+        sfmm_plan& P = S.plan;
+        P.h = h, P.n_targets = nt, P.n_pairs = np, P.n_groups = n_groups, P.n_sources = n_sources;
+        const size_t padded = (size_t)std::max<int64_t>(n_groups, 1) * kPlanGroup;
+        CU(cudaMallocAsync((void**)&P.d_grp_ptr, sizeof(int64_t) * S.grp_ptr.size(), sc));
+        CU(cudaMallocAsync((void**)&P.d_src_index, sizeof(int32_t) * padded, sc));
+        CU(cudaMallocAsync(&P.d_shifts, es * padded * 3, sc));
+        CU(cudaMallocAsync(&P.d_angles, es * padded * 6, sc));
+        CU(S.tgt.alloc(sizeof(int64_t) * (nt + 1)));
+        CU(S.gt.alloc(sizeof(int32_t) * S.grp_target.size()));
+        CU(S.idx.alloc(sizeof(int32_t) * std::max<int64_t>(np, 1)));
+        CU(S.sh.alloc(es * 3 * std::max<int64_t>(np, 1)));
+        CU(S.out.alloc(es * so * S.ostride));
+        CU(S.out_aos.alloc(es * so * std::max<int64_t>(nt, 1)));
+        CU(cudaMemcpyAsync(P.d_grp_ptr, S.grp_ptr.data(), sizeof(int64_t) * S.grp_ptr.size(),
+                           cudaMemcpyHostToDevice, sc));
+        // local_ptr is a temporary: a pageable source is staged before the call returns
+        CU(cudaMemcpyAsync(S.tgt.p, local_ptr.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, sc));
+        CU(cudaMemcpyAsync(S.gt.p, S.grp_target.data(), sizeof(int32_t) * S.grp_target.size(),
+                           cudaMemcpyHostToDevice, sc));
+        if (np > 0) {
+            CU(cudaMemcpyAsync(S.idx.p, src_index + p0, sizeof(int32_t) * np, cudaMemcpyHostToDevice, sc));
+            CU(cudaMemcpyAsync(S.sh.p, shifts + 3 * p0, es * 3 * np, cudaMemcpyHostToDevice, sc));
+        }
+        CU(launch_build_plan<Real>(S.tgt.as<int64_t>(), P.d_grp_ptr, S.gt.as<int32_t>(), S.idx.as<int32_t>(),
+                                   S.sh.as<Real>(), n_groups, n_sources, kPlanGroup, P.d_src_index,
+                                   static_cast<Real*>(P.d_shifts), static_cast<Real*>(P.d_angles),
+                                   d_flags.as<int>() + 2 * k, sc));
+        h->launches += 1;
+        CU(cudaEventCreateWithFlags(&S.ready, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming));
+        CU(cudaEventRecord(S.ready, sc));
+        // compute of the slab on the second stream
+        CU(cudaStreamWaitEvent(sx, S.ready, 0));
+        const sfmm_status st = accumulate_impl<Real>(h, &P, p_in, p_out, d_src.as<Real>(), srows, LAYOUT_ROWS,
+                                                     S.out.as<Real>(), S.ostride, sx);
+        if (st != SFMM_OK) return st;
+        CU(launch_unpack_soa<Real>(S.out.as<Real>(), S.out_aos.as<Real>(), nt, p_out, S.ostride, sx));
+        h->launches += 1;
+        CU(cudaEventRecord(S.done, sx));
+    }
+    // validation of every slab before the first byte of output moves
+    std::vector<int> flags(2 * K, 0);
+    CU(cudaMemcpyAsync(flags.data(), d_flags.p, sizeof(int) * 2 * K, cudaMemcpyDeviceToHost, sc));
+    CU(cudaStreamSynchronize(sc));
+    for (int k = 0; k < K; ++k)
+        if (flags[2 * k]) return fail(SFMM_INVALID_ARGUMENT, "source index out of range");
+    for (int k = 0; k < K; ++k)
+        if (flags[2 * k + 1]) return fail(SFMM_DOMAIN_ERROR, "translation with zero shift vector");
+    // downloads on the (now idle) copy stream, each behind its slab's kernels
+    for (int k = 0; k < K; ++k) {
+        Slab& S = *slabs[k];
+        CU(cudaStreamWaitEvent(sc, S.done, 0));
+        if (S.plan.n_targets > 0)
+            CU(cudaMemcpyAsync(out_aos + S.t0 * so, S.out_aos.p, es * so * S.plan.n_targets,
+                               cudaMemcpyDeviceToHost, sc));
+    }
+    CU(cudaStreamSynchronize(sc));
+    return SFMM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -703,6 +857,11 @@ sfmm_status sfmm_measure_dmma_peak(sfmm_handle* h, double* tflops) {
 
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
     if (!h || !name) return fail(SFMM_INVALID_ARGUMENT, "null handle or option name");
+    if (std::strcmp(name, "level_slab_pairs") == 0) {
+        if (value < 64) return fail(SFMM_INVALID_ARGUMENT, "level_slab_pairs must be >= 64");
+        h->level_slab_pairs = value;
+        return SFMM_OK;
+    }
     if (std::strcmp(name, "kernel_variant") == 0) {
         if (value < 0 || value > 4) return fail(SFMM_INVALID_ARGUMENT, "kernel_variant must be 0..4");
         h->variant = (int)value;
@@ -979,6 +1138,24 @@ sfmm_status sfmm_m2l_accumulate_rows(sfmm_handle* h, const sfmm_plan* plan, int 
                                        rows_off(p_in), LAYOUT_ROWS, (double*)d_out, out_stride, s);
     return accumulate_impl<float>(h, plan, p_in, p_out, (const float*)d_src_rows, rows_off(p_in),
                                   LAYOUT_ROWS, (float*)d_out, out_stride, s);
+}
+
+sfmm_status sfmm_m2l_level_host(sfmm_handle* h, int64_t n_targets, const int64_t* tgt_ptr,
+                                const int32_t* src_index, const void* shifts, int64_t n_sources, int p_in,
+                                int p_out, const void* src_aos, void* out_aos) {
+    if (!h || n_targets < 0 || n_sources < 0 || !tgt_ptr)
+        return fail(SFMM_INVALID_ARGUMENT, "bad level arguments");
+    if (tgt_ptr[0] != 0) return fail(SFMM_INVALID_ARGUMENT, "tgt_ptr[0] must be 0");
+    if ((tgt_ptr[n_targets] > 0 && (!src_index || !shifts)) || !src_aos || !out_aos)
+        return fail(SFMM_INVALID_ARGUMENT, "translation request with null solid");
+    const sfmm_status st = check_orders(h, SFMM_M2L, p_in, p_out);
+    if (st != SFMM_OK) return st;
+    DeviceGuard guard(h->device);
+    if (h->precision == SFMM_F64)
+        return level_host_impl<double>(h, n_targets, tgt_ptr, src_index, (const double*)shifts, n_sources,
+                                       p_in, p_out, (const double*)src_aos, (double*)out_aos);
+    return level_host_impl<float>(h, n_targets, tgt_ptr, src_index, (const float*)shifts, n_sources, p_in,
+                                  p_out, (const float*)src_aos, (float*)out_aos);
 }
 
 sfmm_status sfmm_m2l_accumulate_host(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,

@@ -500,3 +500,36 @@ def test_sharded_level_over_all_visible_devices(oracle, h64):
         lp.close()
         h.close()
     assert bits_equal(np.concatenate(parts), want)
+
+
+def test_one_shot_level_is_the_two_call_form(oracle, h64):
+    """sfmm_m2l_level_host (pipelined over target slabs) against plan + accumulate_host: same
+    bits with 1, 2 and 4 slabs, ragged targets; a failure anywhere leaves the output untouched."""
+    rng = np.random.default_rng(307)
+    ns, p = 40, 10
+    counts = np.array([0, 1, 70, 3, 0, 64, 65, 130, 2, 17, 0, 5, 200, 9])
+    tgt_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    idx = rng.integers(0, ns, int(tgt_ptr[-1])).astype(np.int32)
+    sh = random_shifts(rng, len(idx), with_axes=False)
+    src = random_solids(rng, ns, p)
+    plan = h64.plan(tgt_ptr, idx, sh, ns)
+    want = plan.accumulate_host(p, p, src)
+    plan.close()
+    try:
+        for slab in (1 << 18, 200, 100):          # 1, 2 and 4 slabs for 566 pairs
+            h64.set_option("level_slab_pairs", slab)
+            assert bits_equal(h64.m2l_level_host(tgt_ptr, idx, sh, p, p, src), want), slab
+        h64.set_option("level_slab_pairs", 100)
+        bad = sh.copy()
+        bad[-3] = 0.0                              # in the last slab
+        out = np.full((len(counts), solid_size(p)), 7.0)
+        with pytest.raises(capi.DomainError):
+            h64.m2l_level_host(tgt_ptr, idx, bad, p, p, src, out)
+        assert np.all(out == 7.0)
+        badi = idx.copy()
+        badi[5] = ns + 3
+        with pytest.raises(capi.InvalidArgument):
+            h64.m2l_level_host(tgt_ptr, badi, sh, p, p, src, out)
+        assert np.all(out == 7.0)
+    finally:
+        h64.set_option("level_slab_pairs", 1 << 18)
