@@ -136,7 +136,10 @@ sfmm_status sfmm_pack_rows(sfmm_handle* h, int64_t n, int p, const void* d_aos,
 /* ---- target-owned M2L accumulation (a full interaction-list level) -------
  * L[t] = sum over the sources s of target t of m2l(M[s], shift(t, s)), each
  * term computed exactly as the batched call computes it, summed without
- * atomics in a fixed order. The reference has
+ * atomics in a fixed order that depends only on the order pair and the kernel
+ * variant (sfmm_accumulation_unit below tells which; DESIGN.md "Accumulation
+ * order"): repeated calls give the same bits, different kernels may differ in
+ * the last bits of a sum. The reference has
  * no such entry point (it overwrites: pipeline.cpp:258-265); a caller of the
  * reference issues one request per pair and adds the outputs itself.
  *
