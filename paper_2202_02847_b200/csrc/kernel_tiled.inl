@@ -1056,8 +1056,12 @@ int tiled_warps_for(int p_rot) {
         const int w = atoi(env);
         if (w >= 2 && w <= SFMM_MAXTHREADS / 32) return w;
     }
-    if (p_rot >= 12) return 12;
-    return 4;
+    // measured (profiles/ncu_r02_notes.md, "warps per CTA"): 6 warps wherever two CTAs of 6 fit
+    // an SM (168 registers x 192 threads twice, two triangles in shared memory): double
+    // precision orders 9..14, single precision orders 12..18; 12 warps (one CTA per SM) for
+    // the larger double-precision triangles; 4 warps (three or more CTAs) below
+    if (sizeof(Real) == 8) return p_rot >= 15 ? 12 : (p_rot >= 9 ? 6 : 4);
+    return p_rot >= 12 ? 6 : 4;
 }
 
 }  // namespace
