@@ -606,6 +606,7 @@ struct RowConst {
     int64_t geo_stride;        // geo_elems
     int buf_off;               // element offset of the triangle in smem_raw
     int p_in, p_out, p_rot;
+    const int32_t* grp_target; // accumulate mode, direct form: target of every group, else null
 };
 // per-call flags of elementwise_rows
 enum : int { ROWS_D = 1, ROWS_A = 2, ROWS_PARITY_D = 4, ROWS_PARITY_A = 8, ROWS_MISC_SHIFT = 4 };
@@ -639,6 +640,11 @@ __device__ __forceinline__ void load4_cg(const float* p, float (&x)[4]) {
     x[3] = v.w;
 }
 
+__device__ __forceinline__ void add_ordered(double* dst, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(dst), "d"(v) : "memory");
+}
+__device__ __forceinline__ void add_ordered(float* dst, float v) { __stcg(dst, __ldcg(dst) + v); }
+
 // ROWS: the sources are in LAYOUT_ROWS (sfmm_internal.hpp): a lane reads re, im of two
 // consecutive m of its own source with one load and touches whole sectors only.
 template <int TL, bool ACC, bool ROWS>
@@ -664,6 +670,17 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
     // read the source of the group's first pair, so a non-finite value can only reach a
     // target that the reference poisons as well.
     Real dc1[TL], ds1[TL], ac1[TL], as1[TL];
+    // accumulate mode: column of this group's sums in e.out. Direct form: the target itself;
+    // the groups of a target follow one another in this CTA (barriers in between), every
+    // group after the first adds to what the previous ones left (ascending group order, the
+    // order of reduce_groups_kernel)
+    bool first_d = true;
+    Real* out_d = e.out + g_d;
+    if (ACC && do_d && e.grp_target) {
+        const int32_t tg = e.grp_target[g_d];
+        first_d = g_d == 0 || e.grp_target[g_d - 1] != tg;
+        out_d = e.out + tg;
+    }
     const Real* pa[TL];  // the slot's source: coefficient q at pa[t][q in_stride] (SoA), or
                          // its expansion (ROWS)
     int64_t bd[TL];
@@ -784,8 +801,15 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
                     lane_transpose_sum<NV>(v, lane);
                     // lanes REP k .. REP k + REP-1 hold value k: element k >> 1, part k & 1
                     const int k = lane / REP, m = m0 + (k >> 1), part = k & 1;
-                    if (!(lane & (REP - 1)) && m <= n && !(part && m == 0))
-                        __stcg(e.out + (int64_t)(aos_re(n, m) + part) * e.out_stride + g_d, v[0]);
+                    if (!(lane & (REP - 1)) && m <= n && !(part && m == 0)) {
+                        Real* dst = out_d + (int64_t)(aos_re(n, m) + part) * e.out_stride;
+                        // 0 + first group, as reduce_groups_kernel starts (same signed zeros);
+                        // later groups add at the L2 (no round trip; the store and the
+                        // reductions of one address are ordered by the barriers between the
+                        // groups). red.f32 would flush subnormals: read-modify-write there
+                        if (first_d) __stcg(dst, Real(0) + v[0]);
+                        else add_ordered(dst, v[0]);
+                    }
                 }
             }
         }
@@ -893,14 +917,39 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         rc.p_in = p_in;
         rc.p_out = p_out;
         rc.p_rot = p_rot;
+        rc.grp_target = a.grp_target;
     }
     const int rows_misc = misc_off << ROWS_MISC_SHIFT;
     // warps [0, n_cwarps) start the last phase with the C half tasks, the others with the rows
     const int n_cwarps = W - min(max(tt.row_warps, 0), W - 1);
 
+    // groups of this CTA: strided over the CTAs, or (direct accumulation) all groups of the
+    // targets blockIdx.x, blockIdx.x + gridDim.x, ...: the groups of a target meet in one CTA in
+    // ascending order, and the CTAs work on neighbouring targets at the same time (their
+    // sources are shared through the L2; contiguous target ranges per CTA measured 4 % slower)
+    // (group numbers fit 32 bits: launch_translate_tiled refuses more)
+    constexpr int END = INT_MAX;
+    int walk_t = blockIdx.x, walk_hi = 0;  // direct form: target of the walk, end of its groups
+    auto advance = [&](int g) -> int {
+        if (!a.grp_ptr) {
+            g = g < 0 ? (int)blockIdx.x : g + (int)gridDim.x;
+            return g < (int)n_groups ? g : END;
+        }
+        if (g >= 0 && g + 1 < walk_hi) return g + 1;
+        for (walk_t = g < 0 ? walk_t : walk_t + (int)gridDim.x; walk_t < (int)a.n_targets;
+             walk_t += (int)gridDim.x) {
+            const int lo = (int)a.grp_ptr[walk_t];
+            walk_hi = (int)a.grp_ptr[walk_t + 1];
+            if (lo < walk_hi) return lo;
+        }
+        return END;
+    };
+    const int g_first = advance(-1);
+    int ahead = g_first == END ? END : advance(g_first);  // the group behind `nxt`
     // geometry of the first group; later groups are prepared one group ahead (geometry during
     // the z-step, phase A behind phase D of the same row)
-    geometry_phase<TL>(a, blockIdx.x, p_rot, geo_base, src_local, dst_local, warp, lane);
+    if (g_first != END)
+        geometry_phase<TL>(a, g_first, p_rot, geo_base, src_local, dst_local, warp, lane);
     __syncthreads();
 
     // Schedule (three CTA-wide barriers per group). One trip of the loop:
@@ -915,9 +964,9 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     // The row code is inline at this one place (out of line, called directly, ptxas fits
     // caller and callee into one register budget and spills the loads in flight).
     int parity = 0, gen = 0;  // parity: geometry buffer of `nxt`
-    int64_t cur = -1;
-    for (int64_t nxt = blockIdx.x;; nxt += gridDim.x, parity ^= 1) {
-        const bool has_next = nxt < n_groups;
+    int cur = -1;
+    for (int nxt = g_first;; parity ^= 1) {
+        const bool has_next = nxt != END;
         if (cur >= 0 && warp < n_cwarps) {
             // ---- C of `cur`. Columns >= cols of the z-step output are zero
             // (pipeline.cpp:229-246) and are skipped, which is exact.
@@ -949,7 +998,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         SFMM_PHASE_MARK(4)
 
         const GeoView<TL> gv(geo_base + (size_t)parity * geo_elems<TL>(p_rot) + lane, p_rot);
-        const bool more = nxt + gridDim.x < n_groups;
+        const bool more = ahead != END;
         ++gen;
         if (tab_pending) {
             mbar_wait(mbar, tab_phase);
@@ -979,7 +1028,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
 
         // ---- Z: z-axis step per (column, re|im), longest columns first
         if (more)
-            geometry_phase<TL>(a, nxt + gridDim.x, p_rot,
+            geometry_phase<TL>(a, ahead, p_rot,
                                geo_base + (size_t)(parity ^ 1) * geo_elems<TL>(p_rot), src_local,
                                dst_local, warp, lane);
         for (int task = fetch_task(&counters[1], lane); task < 2 * cols;
@@ -997,6 +1046,8 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         SFMM_PHASE_MARK(3)
         if (threadIdx.x == 0) counters[1] = 0;
         cur = nxt;
+        nxt = ahead;
+        if (ahead != END) ahead = advance(ahead);
     }
 #undef SFMM_PHASE_MARK
 }
@@ -1087,6 +1138,7 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     const TiledLayout<TL> lay{p_rot, tab_len};
     const size_t smem = lay.smem_bytes();
     const int64_t n_groups = (a.n + L - 1) / L;
+    if (n_groups >= INT_MAX || a.n_targets >= INT_MAX) return cudaErrorInvalidValue;
     const int block = 32 * tiled_warps_for(p_rot);
     const bool acc = a.src_index != nullptr, rows = a.in_layout == LAYOUT_ROWS;
     auto kern = acc ? (rows ? translate_tiled_kernel<TL, true, true> : translate_tiled_kernel<TL, true, false>)

@@ -119,6 +119,8 @@ struct sfmm_plan {
     int32_t* d_src_index = nullptr; // [n_groups * 64], -1 = idle lane
     void* d_shifts = nullptr;       // [n_groups * 64][3]
     void* d_angles = nullptr;       // [6][n_groups * 64]: decomposed shifts (TranslateArgs::angles)
+    int32_t* d_grp_target = nullptr; // [n_groups]: target of every group
+    int64_t max_groups = 0;         // most groups of one target
     cudaStream_t last_stream = nullptr;  // stream of the most recent accumulate call (destroy order)
 };
 
@@ -453,6 +455,8 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
         grp_ptr[(size_t)t + 1] = grp_ptr[(size_t)t] + (cnt + kPlanGroup - 1) / kPlanGroup;
     }
     const int64_t n_groups = grp_ptr[(size_t)n_targets];
+    for (int64_t t = 0; t < n_targets; ++t)
+        plan->max_groups = std::max(plan->max_groups, grp_ptr[(size_t)t + 1] - grp_ptr[(size_t)t]);
     std::vector<int32_t> grp_target((size_t)std::max<int64_t>(n_groups, 1));
     for (int64_t t = 0; t < n_targets; ++t)
         for (int64_t g = grp_ptr[(size_t)t]; g < grp_ptr[(size_t)t + 1]; ++g)
@@ -473,11 +477,11 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
     CU(cudaMallocAsync((void**)&plan->d_src_index, sizeof(int32_t) * padded, stream));
     CU(cudaMallocAsync(&plan->d_shifts, sizeof(Real) * padded * 3, stream));
     CU(cudaMallocAsync(&plan->d_angles, sizeof(Real) * padded * 6, stream));
+    CU(cudaMallocAsync((void**)&plan->d_grp_target, sizeof(int32_t) * grp_target.size(), stream));
     plan->last_stream = stream;
-    DevBuf d_tgt(stream), d_gt(stream), d_idx(stream), d_sh(stream), d_flags(stream);
+    DevBuf d_tgt(stream), d_idx(stream), d_sh(stream), d_flags(stream);
     const size_t np = (size_t)std::max<int64_t>(n_pairs, 1);
     CU(d_tgt.alloc(sizeof(int64_t) * (n_targets + 1)));
-    CU(d_gt.alloc(sizeof(int32_t) * grp_target.size()));
     CU(d_idx.alloc(sizeof(int32_t) * np));
     CU(d_sh.alloc(sizeof(Real) * np * 3));
     CU(d_flags.alloc(sizeof(int) * 2));
@@ -486,7 +490,7 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
                        cudaMemcpyHostToDevice, stream));
     CU(cudaMemcpyAsync(d_tgt.p, tgt_ptr, sizeof(int64_t) * (n_targets + 1), cudaMemcpyHostToDevice,
                        stream));
-    CU(cudaMemcpyAsync(d_gt.p, grp_target.data(), sizeof(int32_t) * grp_target.size(),
+    CU(cudaMemcpyAsync(plan->d_grp_target, grp_target.data(), sizeof(int32_t) * grp_target.size(),
                        cudaMemcpyHostToDevice, stream));
     if (n_pairs > 0) {
         CU(cudaMemcpyAsync(d_idx.p, src_index, sizeof(int32_t) * n_pairs, cudaMemcpyHostToDevice,
@@ -494,7 +498,7 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
         CU(cudaMemcpyAsync(d_sh.p, shifts, sizeof(Real) * n_pairs * 3, cudaMemcpyHostToDevice,
                            stream));
     }
-    CU(launch_build_plan<Real>(d_tgt.as<int64_t>(), plan->d_grp_ptr, d_gt.as<int32_t>(),
+    CU(launch_build_plan<Real>(d_tgt.as<int64_t>(), plan->d_grp_ptr, plan->d_grp_target,
                                d_idx.as<int32_t>(), d_sh.as<Real>(), n_groups, n_sources, kPlanGroup,
                                plan->d_src_index, static_cast<Real*>(plan->d_shifts),
                                static_cast<Real*>(plan->d_angles), d_flags.as<int>(), stream));
@@ -521,23 +525,42 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.in_layout = src_layout;
     if (translate_variant<Real>(tables_of<Real>(h), a) == 0)
         return fail(SFMM_INVALID_ARGUMENT, "the selected kernel variant does not apply to this call");
+    a.in = d_src;
+    a.in_stride = src_stride;
+    a.shifts = static_cast<const Real*>(plan->d_shifts);
+    a.angles = static_cast<const Real*>(plan->d_angles);
+    a.n = plan->n_groups * kPlanGroup;
+    a.phase_clocks = h->d_phase_clocks;
+    // tiled kernel, direct form: a CTA owns whole targets and adds their groups itself. Not for
+    // lists with a target so long that its CTA would run on alone (more than 1/8 of a CTA's
+    // share of the groups): those take the partial sums + reduce_groups_kernel path below
+    const bool direct = translate_variant<Real>(tables_of<Real>(h), a) == 2 && plan->d_grp_target &&
+                        (plan->max_groups <= 4 ||
+                         plan->max_groups * 8 * (int64_t)h->sm_count <= plan->n_groups);
+    if (direct) {
+        const_cast<sfmm_plan*>(plan)->last_stream = stream;
+        a.out = d_out;
+        a.out_stride = out_stride;
+        a.grp_target = plan->d_grp_target;
+        a.grp_ptr = plan->d_grp_ptr;
+        a.n_targets = plan->n_targets;
+        cudaError_t e = launch_zero_unwritten<Real>(plan->d_grp_ptr, plan->n_targets, p_out, d_out,
+                                                    out_stride, stream);
+        LaunchInfo info;
+        if (e == cudaSuccess && a.n > 0)
+            e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
+        h->launches += 1 + info.launches;
+        if (e != cudaSuccess) return cuda_fail(e, "m2l_accumulate");
+        return SFMM_OK;
+    }
     // the kernel reduces the lanes of one of ITS groups (16, 32 or 64 pairs) into one partial
     const int per = kPlanGroup / translate_group_size<Real>(tables_of<Real>(h), a);
     const int64_t n_partial = plan->n_groups * per;
     DevBuf partial(stream);
     if (n_partial > 0) CU(partial.alloc(sizeof(Real) * so * n_partial));
     const_cast<sfmm_plan*>(plan)->last_stream = stream;
-    a.n = plan->n_groups * kPlanGroup;
-    a.in = d_src;
-    a.in_stride = src_stride;
-    a.in_layout = src_layout;
-    a.shifts = static_cast<const Real*>(plan->d_shifts);
-    a.angles = static_cast<const Real*>(plan->d_angles);
     a.out = partial.as<Real>();
     a.out_stride = n_partial;
-    a.src_index = plan->d_src_index;
-    a.variant = h->variant;
-    a.phase_clocks = h->d_phase_clocks;
     LaunchInfo info;
     cudaError_t e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
     h->launches += info.launches;
@@ -594,6 +617,7 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
         if (plan.d_src_index) cudaFreeAsync(plan.d_src_index, s);
         if (plan.d_shifts) cudaFreeAsync(plan.d_shifts, s);
         if (plan.d_angles) cudaFreeAsync(plan.d_angles, s);
+        if (plan.d_grp_target) cudaFreeAsync(plan.d_grp_target, s);
         return st;
     }
     for (int64_t t = 0; t < n_targets; ++t)
@@ -610,10 +634,10 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
         sfmm_plan plan;
         std::vector<int64_t> grp_ptr;
         std::vector<int32_t> grp_target;
-        DevBuf tgt, gt, idx, sh, out, out_aos;
+        DevBuf tgt, idx, sh, out, out_aos;
         cudaEvent_t ready = nullptr, done = nullptr;
         int64_t t0 = 0, ostride = 0;
-        explicit Slab(cudaStream_t c, cudaStream_t x) : tgt(c), gt(c), idx(c), sh(c), out(x), out_aos(x) {}
+        explicit Slab(cudaStream_t c, cudaStream_t x) : tgt(c), idx(c), sh(c), out(x), out_aos(x) {}
     };
     // declared before the guard below: the guard drains the streams first, then the buffers go
     DevBuf d_src_aos(sc), d_src(sc), d_flags(sc);
@@ -634,6 +658,7 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
                 if (p.d_src_index) cudaFreeAsync(p.d_src_index, a);
                 if (p.d_shifts) cudaFreeAsync(p.d_shifts, a);
                 if (p.d_angles) cudaFreeAsync(p.d_angles, a);
+                if (p.d_grp_target) cudaFreeAsync(p.d_grp_target, a);
             }
             if (*ev) cudaEventDestroy(*ev);
         }
@@ -669,13 +694,15 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
         for (int64_t t = 0; t <= nt; ++t) local_ptr[(size_t)t] = tgt_ptr[t0 + t] - p0;
         sfmm_plan& P = S.plan;
         P.h = h, P.n_targets = nt, P.n_pairs = np, P.n_groups = n_groups, P.n_sources = n_sources;
+        for (int64_t t = 0; t < nt; ++t)
+            P.max_groups = std::max(P.max_groups, S.grp_ptr[(size_t)t + 1] - S.grp_ptr[(size_t)t]);
         const size_t padded = (size_t)std::max<int64_t>(n_groups, 1) * kPlanGroup;
         CU(cudaMallocAsync((void**)&P.d_grp_ptr, sizeof(int64_t) * S.grp_ptr.size(), sc));
         CU(cudaMallocAsync((void**)&P.d_src_index, sizeof(int32_t) * padded, sc));
         CU(cudaMallocAsync(&P.d_shifts, es * padded * 3, sc));
         CU(cudaMallocAsync(&P.d_angles, es * padded * 6, sc));
+        CU(cudaMallocAsync((void**)&P.d_grp_target, sizeof(int32_t) * S.grp_target.size(), sc));
         CU(S.tgt.alloc(sizeof(int64_t) * (nt + 1)));
-        CU(S.gt.alloc(sizeof(int32_t) * S.grp_target.size()));
         CU(S.idx.alloc(sizeof(int32_t) * std::max<int64_t>(np, 1)));
         CU(S.sh.alloc(es * 3 * std::max<int64_t>(np, 1)));
         CU(S.out.alloc(es * so * S.ostride));
@@ -684,13 +711,13 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
                            cudaMemcpyHostToDevice, sc));
         // local_ptr is a temporary: a pageable source is staged before the call returns
         CU(cudaMemcpyAsync(S.tgt.p, local_ptr.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, sc));
-        CU(cudaMemcpyAsync(S.gt.p, S.grp_target.data(), sizeof(int32_t) * S.grp_target.size(),
+        CU(cudaMemcpyAsync(P.d_grp_target, S.grp_target.data(), sizeof(int32_t) * S.grp_target.size(),
                            cudaMemcpyHostToDevice, sc));
         if (np > 0) {
             CU(cudaMemcpyAsync(S.idx.p, src_index + p0, sizeof(int32_t) * np, cudaMemcpyHostToDevice, sc));
             CU(cudaMemcpyAsync(S.sh.p, shifts + 3 * p0, es * 3 * np, cudaMemcpyHostToDevice, sc));
         }
-        CU(launch_build_plan<Real>(S.tgt.as<int64_t>(), P.d_grp_ptr, S.gt.as<int32_t>(), S.idx.as<int32_t>(),
+        CU(launch_build_plan<Real>(S.tgt.as<int64_t>(), P.d_grp_ptr, P.d_grp_target, S.idx.as<int32_t>(),
                                    S.sh.as<Real>(), n_groups, n_sources, kPlanGroup, P.d_src_index,
                                    static_cast<Real*>(P.d_shifts), static_cast<Real*>(P.d_angles),
                                    d_flags.as<int>() + 2 * k, sc));
@@ -1095,6 +1122,7 @@ void sfmm_plan_destroy(sfmm_plan* plan) {
         if (plan->d_src_index) cudaFreeAsync(plan->d_src_index, s);
         if (plan->d_shifts) cudaFreeAsync(plan->d_shifts, s);
         if (plan->d_angles) cudaFreeAsync(plan->d_angles, s);
+        if (plan->d_grp_target) cudaFreeAsync(plan->d_grp_target, s);
     }
     delete plan;
 }

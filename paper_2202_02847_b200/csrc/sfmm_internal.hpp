@@ -58,6 +58,12 @@ struct TranslateArgs {
     Real* out = nullptr;          // SoA [c][out_stride]; accumulate mode: partials [c][n/32]
     int64_t out_stride = 0;
     const int32_t* src_index = nullptr;  // accumulate mode: source per lane, -1 = idle lane
+    // accumulate mode, direct form (tiled kernel): `out` is the final SoA output [c][target];
+    // a CTA works on a contiguous, target-aligned range of groups and adds the groups of a
+    // target in ascending order itself (no partial buffer, no reduce kernel)
+    const int32_t* grp_target = nullptr;  // [n / 64] target of every group
+    const int64_t* grp_ptr = nullptr;     // [n_targets + 1] first group of every target
+    int64_t n_targets = 0;
     const int* fail_flag = nullptr;      // device int; non-zero -> kernel writes nothing
     int variant = 0;                     // 0 auto, 1 generic, 2 tiled, 3 mma, 4 small-order kernel
     long long* phase_clocks = nullptr;   // optional [8] cycle counters of CTA 0 (tuning aid)
@@ -135,6 +141,12 @@ cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
                               const Real* shifts, int64_t n_groups, int64_t n_sources, int group,
                               int32_t* out_index, Real* out_shifts, Real* out_angles, int* flags,
                               cudaStream_t stream);
+
+// Accumulate mode, direct form: zeroes what the translation kernel does not write (the
+// Im(C_n^0) planes of every target, all planes of targets without pairs).
+template <typename Real>
+cudaError_t launch_zero_unwritten(const int64_t* grp_ptr, int64_t n_targets, int p_out, Real* out,
+                                  int64_t out_stride, cudaStream_t stream);
 
 // Accumulate mode, second stage: out[c][t] = sum_{g in groups of t} partial[c][g],
 // groups in ascending order. grp_ptr: [n_targets + 1] in units of `per` partial groups.

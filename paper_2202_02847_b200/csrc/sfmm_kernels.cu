@@ -117,6 +117,18 @@ __global__ void reduce_groups_kernel(const Real* __restrict__ partial, int64_t n
     out[(int64_t)c * out_stride + t] = acc;
 }
 
+template <typename Real>
+__global__ void zero_unwritten_kernel(const int64_t* __restrict__ grp_ptr, int64_t n_targets, int P,
+                                      Real* __restrict__ out, int64_t out_stride) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_targets) return;
+    if (grp_ptr[t + 1] == grp_ptr[t]) {
+        for (int c = 0; c < P * (P + 1); ++c) out[(int64_t)c * out_stride + t] = Real(0);
+    } else {
+        for (int n = 0; n < P; ++n) out[(int64_t)(aos_re(n, 0) + 1) * out_stride + t] = Real(0);
+    }
+}
+
 // FMA-pipe peak probe (roofline denominator measured next to the benchmark).
 template <typename Real>
 __global__ void fma_peak_kernel(Real* out, int iters, Real a, Real b) {
@@ -289,6 +301,15 @@ cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
 }
 
 template <typename Real>
+cudaError_t launch_zero_unwritten(const int64_t* grp_ptr, int64_t n_targets, int p_out, Real* out,
+                                  int64_t out_stride, cudaStream_t stream) {
+    if (n_targets <= 0) return cudaSuccess;
+    zero_unwritten_kernel<Real><<<(unsigned)((n_targets + 127) / 128), 128, 0, stream>>>(
+        grp_ptr, n_targets, p_out, out, out_stride);
+    return cudaGetLastError();
+}
+
+template <typename Real>
 cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const int64_t* grp_ptr,
                                  int per, int64_t n_targets, int p_out, Real* out,
                                  int64_t out_stride, cudaStream_t stream) {
@@ -405,6 +426,8 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
     template cudaError_t launch_pack_rows<Real>(const Real*, Real*, int64_t, int, cudaStream_t); \
     template cudaError_t launch_unpack_soa<Real>(const Real*, Real*, int64_t, int, int64_t,     \
                                                  cudaStream_t);                                 \
+    template cudaError_t launch_zero_unwritten<Real>(const int64_t*, int64_t, int, Real*, int64_t,  \
+                                                     cudaStream_t);                             \
     template cudaError_t launch_reduce_groups<Real>(const Real*, int64_t, const int64_t*, int,  \
                                                     int64_t, int, Real*, int64_t, cudaStream_t); \
     template int translate_variant<Real>(const DeviceTables<Real>&, const TranslateArgs<Real>&); \

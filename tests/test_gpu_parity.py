@@ -329,6 +329,27 @@ def test_accumulation_mixed_orders(oracle, h64):
         plan.close()
 
 
+def test_accumulation_many_ragged_targets_and_long_targets(oracle, h64, h32):
+    """More targets than CTAs with ragged pair counts (the tiled kernel walks whole targets,
+    strided over the CTAs, and adds their groups itself), and lists with one very long
+    target (partial sums + reduce kernel instead): both bit-exact in the documented order."""
+    rng = np.random.default_rng(131)
+    ns = 60
+    for h, p, dt in ((h64, 6, np.float64), (h32, 5, np.float32), (h64, 11, np.float64)):
+        for counts in (rng.integers(0, 200, 700), np.array([5, 1500, 0, 64, 129]),
+                       np.concatenate([rng.integers(0, 70, 300), [900]])):
+            tgt_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+            idx = rng.integers(0, ns, int(tgt_ptr[-1])).astype(np.int32)
+            sh = random_shifts(rng, len(idx), with_axes=False).astype(dt)
+            src = random_solids(rng, ns, p).astype(dt)
+            plan = h.plan(tgt_ptr, idx, sh, ns)
+            got = plan.accumulate_host(p, p, src)
+            plan.close()
+            _, per_pair = oracle.translate("m2l", p, p, src[idx], sh, dt)
+            want = sharding.accumulation_tree(per_pair, tgt_ptr, h.accumulation_unit(p, p))
+            assert bits_equal(got, want), (p, len(counts))
+
+
 # ---- API contracts ---------------------------------------------------------
 
 def test_error_contracts(h64):
