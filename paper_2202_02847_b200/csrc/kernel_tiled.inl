@@ -506,12 +506,13 @@ __device__ __forceinline__ void geometry_phase(const TranslateArgs<Real>& a, int
     Angles<Real> ang;
     Real inv;
     if (a.angles) {  // plan path: decomposed when the plan was built, for every padded lane
-        ang.rn = a.angles[b];
-        ang.ca = a.angles[a.n + b];
-        ang.sa = a.angles[2 * a.n + b];
-        ang.cb = a.angles[3 * a.n + b];
-        ang.sb = a.angles[4 * a.n + b];
-        inv = a.angles[5 * a.n + b];
+        const int64_t j = a.angle_index ? (int64_t)a.angle_index[b] : b;
+        ang.rn = a.angles[j];
+        ang.ca = a.angles[a.n + j];
+        ang.sa = a.angles[2 * a.n + j];
+        ang.cb = a.angles[3 * a.n + j];
+        ang.sb = a.angles[4 * a.n + j];
+        inv = a.angles[5 * a.n + j];
     } else {
         bool active = b < a.n;
         if (active && a.src_index) active = a.src_index[b] >= 0;

@@ -118,7 +118,9 @@ struct sfmm_plan {
     int64_t* d_grp_ptr = nullptr;   // [n_targets + 1]
     int32_t* d_src_index = nullptr; // [n_groups * 64], -1 = idle lane
     void* d_shifts = nullptr;       // [n_groups * 64][3]
-    void* d_angles = nullptr;       // [6][n_groups * 64]: decomposed shifts (TranslateArgs::angles)
+    void* d_angles = nullptr;       // [6][n_groups * 64]: decomposed shifts (TranslateArgs::angles), one
+                                    // entry per distinct shift at the front (or one per lane)
+    int32_t* d_angle_index = nullptr; // [n_groups * 64]: entry of every lane
     int32_t* d_grp_target = nullptr; // [n_groups]: target of every group
     int64_t max_groups = 0;         // most groups of one target
     cudaStream_t last_stream = nullptr;  // stream of the most recent accumulate call (destroy order)
@@ -477,6 +479,7 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
     CU(cudaMallocAsync((void**)&plan->d_src_index, sizeof(int32_t) * padded, stream));
     CU(cudaMallocAsync(&plan->d_shifts, sizeof(Real) * padded * 3, stream));
     CU(cudaMallocAsync(&plan->d_angles, sizeof(Real) * padded * 6, stream));
+    CU(cudaMallocAsync((void**)&plan->d_angle_index, sizeof(int32_t) * padded, stream));
     CU(cudaMallocAsync((void**)&plan->d_grp_target, sizeof(int32_t) * grp_target.size(), stream));
     plan->last_stream = stream;
     DevBuf d_tgt(stream), d_idx(stream), d_sh(stream), d_flags(stream);
@@ -501,8 +504,9 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
     CU(launch_build_plan<Real>(d_tgt.as<int64_t>(), plan->d_grp_ptr, plan->d_grp_target,
                                d_idx.as<int32_t>(), d_sh.as<Real>(), n_groups, n_sources, kPlanGroup,
                                plan->d_src_index, static_cast<Real*>(plan->d_shifts),
-                               static_cast<Real*>(plan->d_angles), d_flags.as<int>(), stream));
-    h->launches += 1;
+                               static_cast<Real*>(plan->d_angles), plan->d_angle_index,
+                               d_flags.as<int>(), stream));
+    h->launches += 4;
     int flags[2] = {0, 0};
     CU(cudaMemcpyAsync(flags, d_flags.p, sizeof(flags), cudaMemcpyDeviceToHost, stream));
     CU(cudaStreamSynchronize(stream));
@@ -529,6 +533,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.in_stride = src_stride;
     a.shifts = static_cast<const Real*>(plan->d_shifts);
     a.angles = static_cast<const Real*>(plan->d_angles);
+    a.angle_index = plan->d_angle_index;
     a.n = plan->n_groups * kPlanGroup;
     a.phase_clocks = h->d_phase_clocks;
     // tiled kernel, direct form: a CTA owns whole targets and adds their groups itself. Not for
@@ -617,6 +622,7 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
         if (plan.d_src_index) cudaFreeAsync(plan.d_src_index, s);
         if (plan.d_shifts) cudaFreeAsync(plan.d_shifts, s);
         if (plan.d_angles) cudaFreeAsync(plan.d_angles, s);
+        if (plan.d_angle_index) cudaFreeAsync(plan.d_angle_index, s);
         if (plan.d_grp_target) cudaFreeAsync(plan.d_grp_target, s);
         return st;
     }
@@ -658,6 +664,7 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
                 if (p.d_src_index) cudaFreeAsync(p.d_src_index, a);
                 if (p.d_shifts) cudaFreeAsync(p.d_shifts, a);
                 if (p.d_angles) cudaFreeAsync(p.d_angles, a);
+                if (p.d_angle_index) cudaFreeAsync(p.d_angle_index, a);
                 if (p.d_grp_target) cudaFreeAsync(p.d_grp_target, a);
             }
             if (*ev) cudaEventDestroy(*ev);
@@ -701,6 +708,7 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
         CU(cudaMallocAsync((void**)&P.d_src_index, sizeof(int32_t) * padded, sc));
         CU(cudaMallocAsync(&P.d_shifts, es * padded * 3, sc));
         CU(cudaMallocAsync(&P.d_angles, es * padded * 6, sc));
+        CU(cudaMallocAsync((void**)&P.d_angle_index, sizeof(int32_t) * padded, sc));
         CU(cudaMallocAsync((void**)&P.d_grp_target, sizeof(int32_t) * S.grp_target.size(), sc));
         CU(S.tgt.alloc(sizeof(int64_t) * (nt + 1)));
         CU(S.idx.alloc(sizeof(int32_t) * std::max<int64_t>(np, 1)));
@@ -720,8 +728,8 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
         CU(launch_build_plan<Real>(S.tgt.as<int64_t>(), P.d_grp_ptr, P.d_grp_target, S.idx.as<int32_t>(),
                                    S.sh.as<Real>(), n_groups, n_sources, kPlanGroup, P.d_src_index,
                                    static_cast<Real*>(P.d_shifts), static_cast<Real*>(P.d_angles),
-                                   d_flags.as<int>() + 2 * k, sc));
-        h->launches += 1;
+                                   P.d_angle_index, d_flags.as<int>() + 2 * k, sc));
+        h->launches += 4;
         CU(cudaEventCreateWithFlags(&S.ready, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming));
         CU(cudaEventRecord(S.ready, sc));
@@ -1122,6 +1130,7 @@ void sfmm_plan_destroy(sfmm_plan* plan) {
         if (plan->d_src_index) cudaFreeAsync(plan->d_src_index, s);
         if (plan->d_shifts) cudaFreeAsync(plan->d_shifts, s);
         if (plan->d_angles) cudaFreeAsync(plan->d_angles, s);
+        if (plan->d_angle_index) cudaFreeAsync(plan->d_angle_index, s);
         if (plan->d_grp_target) cudaFreeAsync(plan->d_grp_target, s);
     }
     delete plan;

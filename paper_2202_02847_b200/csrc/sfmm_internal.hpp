@@ -55,6 +55,8 @@ struct TranslateArgs {
     // optional, plan path: the decomposed shifts [6][n] = |r|, cos/sin alpha, cos/sin beta,
     // 1/|r| (geometry.cpp:11-30), computed once when the plan is built
     const Real* angles = nullptr;
+    // entry of every lane in `angles` (one entry per distinct shift); null: entry = lane
+    const int32_t* angle_index = nullptr;
     Real* out = nullptr;          // SoA [c][out_stride]; accumulate mode: partials [c][n/32]
     int64_t out_stride = 0;
     const int32_t* src_index = nullptr;  // accumulate mode: source per lane, -1 = idle lane
@@ -139,8 +141,8 @@ template <typename Real>
 cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
                               const int32_t* grp_target, const int32_t* src_index,
                               const Real* shifts, int64_t n_groups, int64_t n_sources, int group,
-                              int32_t* out_index, Real* out_shifts, Real* out_angles, int* flags,
-                              cudaStream_t stream);
+                              int32_t* out_index, Real* out_shifts, Real* out_angles,
+                              int32_t* out_angle_index, int* flags, cudaStream_t stream);
 
 // Accumulate mode, direct form: zeroes what the translation kernel does not write (the
 // Im(C_n^0) planes of every target, all planes of targets without pairs).

@@ -61,8 +61,7 @@ __global__ void build_plan_kernel(const int64_t* __restrict__ tgt_ptr,
                                   const int32_t* __restrict__ src_index,
                                   const Real* __restrict__ shifts, int64_t n_groups,
                                   int64_t n_sources, int group, int32_t* __restrict__ out_index,
-                                  Real* __restrict__ out_shifts, Real* __restrict__ out_angles,
-                                  int* flags) {
+                                  Real* __restrict__ out_shifts, int* flags) {
     const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (d >= n_groups * group) return;
     const int64_t g = d / group;
@@ -85,16 +84,93 @@ __global__ void build_plan_kernel(const int64_t* __restrict__ tgt_ptr,
     out_shifts[3 * d] = x;
     out_shifts[3 * d + 1] = y;
     out_shifts[3 * d + 2] = z;
-    // the decomposition the translation kernel would do per group (idle lanes: the benign
-    // shift (0, 0, 1)), with the same device code
-    const Angles<Real> ang = decompose_angles(x, y, z);
-    const int64_t n = n_groups * group;
-    out_angles[d] = ang.rn;
-    out_angles[n + d] = ang.ca;
-    out_angles[2 * n + d] = ang.sa;
-    out_angles[3 * n + d] = ang.cb;
-    out_angles[4 * n + d] = ang.sb;
-    out_angles[5 * n + d] = Real(1) / ang.rn;
+}
+
+// ---- plan geometry: one decomposition per DISTINCT shift ------------------------------------
+// A level of a uniform octree has a few hundred distinct shifts for millions of pairs; the
+// decomposed shifts (geometry.cpp:11-30) are stored once per distinct shift and every lane
+// carries an index (4 bytes instead of 6 reals of DRAM traffic per pair and launch). Shifts are
+// compared by bit pattern. Lists with more distinct shifts than the table holds fall back to
+// one entry per lane (angle_index = identity); the choice is made on the device, so the
+// plan-building stream never waits for the host.
+constexpr int kDedupSlots = 1 << 16;   // open-addressing table of representative lanes
+constexpr int kDedupProbes = 64;
+
+template <typename Real>
+__device__ __forceinline__ bool same_shift(const Real* s, int64_t a, int64_t b) {
+    using Bits = typename std::conditional<sizeof(Real) == 8, unsigned long long, unsigned int>::type;
+    const Bits* u = reinterpret_cast<const Bits*>(s);
+    return u[3 * a] == u[3 * b] && u[3 * a + 1] == u[3 * b + 1] && u[3 * a + 2] == u[3 * b + 2];
+}
+
+// rep[d] = lane whose shift equals that of lane d and that won the table slot; state[1] is
+// raised when the list does not fit
+template <typename Real>
+__global__ void dedup_rep_kernel(const Real* __restrict__ shifts, int64_t n, int* table,
+                                 int32_t* __restrict__ rep, int* state) {
+    const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (d >= n) return;
+    unsigned long long h = 0x9E3779B97F4A7C15ull;
+    for (int k = 0; k < 3; ++k) {
+        unsigned long long v;
+        if (sizeof(Real) == 8) v = (unsigned long long)__double_as_longlong((double)shifts[3 * d + k]);
+        else v = (unsigned long long)__float_as_uint((float)shifts[3 * d + k]);
+        h = (h ^ v) * 0xFF51AFD7ED558CCDull;
+        h ^= h >> 29;
+    }
+    unsigned slot = (unsigned)(h >> 20) & (kDedupSlots - 1);
+    int32_t r = -1;
+    for (int probe = 0; probe < kDedupProbes; ++probe) {
+        const int cur = atomicCAS(&table[slot], -1, (int)d);
+        if (cur == -1) {
+            r = (int32_t)d;
+            break;
+        }
+        if (same_shift(shifts, d, (int64_t)cur)) {
+            r = cur;
+            break;
+        }
+        slot = (slot + 1) & (kDedupSlots - 1);
+    }
+    if (r < 0) {
+        state[1] = 1;
+        r = (int32_t)d;
+    }
+    rep[d] = r;
+}
+
+// representatives take a slot of the compact table and decompose their shift into it; when
+// the list did not fit, every lane decomposes its own shift (slot = lane)
+template <typename Real>
+__global__ void dedup_assign_kernel(const Real* __restrict__ shifts, int64_t n,
+                                    const int32_t* __restrict__ rep, int32_t* __restrict__ uid,
+                                    Real* __restrict__ angles, int* state) {
+    const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (d >= n) return;
+    const bool per_lane = state[1] != 0;
+    int64_t slot = d;
+    if (!per_lane) {
+        if (rep[d] != d) return;
+        const int id = atomicAdd(&state[0], 1);
+        slot = id;
+        uid[d] = id;
+    }
+    const Angles<Real> ang = decompose_angles(shifts[3 * d], shifts[3 * d + 1], shifts[3 * d + 2]);
+    angles[slot] = ang.rn;
+    angles[n + slot] = ang.ca;
+    angles[2 * n + slot] = ang.sa;
+    angles[3 * n + slot] = ang.cb;
+    angles[4 * n + slot] = ang.sb;
+    angles[5 * n + slot] = Real(1) / ang.rn;
+}
+
+template <typename Real>
+__global__ void dedup_index_kernel(int64_t n, const int32_t* __restrict__ rep,
+                                   const int32_t* __restrict__ uid, int32_t* __restrict__ angle_index,
+                                   const int* state) {
+    const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (d >= n) return;
+    angle_index[d] = state[1] ? (int32_t)d : uid[rep[d]];
 }
 
 template <typename Real>
@@ -289,15 +365,36 @@ template <typename Real>
 cudaError_t launch_build_plan(const int64_t* tgt_ptr, const int64_t* grp_ptr,
                               const int32_t* grp_target, const int32_t* src_index,
                               const Real* shifts, int64_t n_groups, int64_t n_sources, int group,
-                              int32_t* out_index, Real* out_shifts, Real* out_angles, int* flags,
-                              cudaStream_t stream) {
+                              int32_t* out_index, Real* out_shifts, Real* out_angles,
+                              int32_t* out_angle_index, int* flags, cudaStream_t stream) {
     if (n_groups <= 0) return cudaSuccess;
     const int block = 256;
-    const int64_t grid = (n_groups * group + block - 1) / block;
+    const int64_t n = n_groups * group;
+    const int64_t grid = (n + block - 1) / block;
     build_plan_kernel<Real><<<(unsigned)grid, block, 0, stream>>>(
         tgt_ptr, grp_ptr, grp_target, src_index, shifts, n_groups, n_sources, group, out_index,
-        out_shifts, out_angles, flags);
-    return cudaGetLastError();
+        out_shifts, flags);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // geometry per distinct shift: {table, rep, uid, state} are stream-ordered temporaries
+    int* scratch = nullptr;
+    const size_t words = (size_t)kDedupSlots + 2 * (size_t)n + 4;
+    e = cudaMallocAsync((void**)&scratch, sizeof(int) * words, stream);
+    if (e != cudaSuccess) return e;
+    int* table = scratch;
+    int32_t* rep = scratch + kDedupSlots;
+    int32_t* uid = rep + n;
+    int* state = uid + n;
+    e = cudaMemsetAsync(table, 0xFF, sizeof(int) * kDedupSlots, stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(int) * 4, stream);
+    if (e == cudaSuccess) {
+        dedup_rep_kernel<Real><<<(unsigned)grid, block, 0, stream>>>(out_shifts, n, table, rep, state);
+        dedup_assign_kernel<Real><<<(unsigned)grid, block, 0, stream>>>(out_shifts, n, rep, uid, out_angles, state);
+        dedup_index_kernel<Real><<<(unsigned)grid, block, 0, stream>>>(n, rep, uid, out_angle_index, state);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(scratch, stream);
+    return e;
 }
 
 template <typename Real>
@@ -435,7 +532,8 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
                                             const TranslateArgs<Real>&);                        \
     template cudaError_t launch_build_plan<Real>(const int64_t*, const int64_t*, const int32_t*, \
                                                  const int32_t*, const Real*, int64_t, int64_t, \
-                                                 int, int32_t*, Real*, Real*, int*, cudaStream_t);     \
+                                                 int, int32_t*, Real*, Real*, int32_t*, int*,          \
+                                                 cudaStream_t);                                 \
     template cudaError_t launch_translate<Real>(const DeviceTables<Real>&,                      \
                                                 const TranslateArgs<Real>&, int, cudaStream_t,  \
                                                 LaunchInfo*);

@@ -539,12 +539,13 @@ __device__ __forceinline__ LaneGeo load_geo(const TranslateArgs<double>& a, int6
     LaneGeo g;
     if (a.angles) {
         if (valid) {
-            g.rn = a.angles[b];
-            g.ca = a.angles[a.n + b];
-            g.sa = a.angles[2 * a.n + b];
-            g.cb = a.angles[3 * a.n + b];
-            g.sb = a.angles[4 * a.n + b];
-            g.inv = a.angles[5 * a.n + b];
+            const int64_t j = a.angle_index ? (int64_t)a.angle_index[b] : b;
+            g.rn = a.angles[j];
+            g.ca = a.angles[a.n + j];
+            g.sa = a.angles[2 * a.n + j];
+            g.cb = a.angles[3 * a.n + j];
+            g.sb = a.angles[4 * a.n + j];
+            g.inv = a.angles[5 * a.n + j];
             return g;
         }
         g.rn = 1, g.ca = 1, g.sa = 0, g.cb = 1, g.sb = -0.0, g.inv = 1;
@@ -609,6 +610,7 @@ struct RowConst {
     int64_t n;
     const double* shifts;
     const double* angles;
+    const int32_t* angle_index;
     int kind, p_in, p_out, pad;
 };
 
@@ -621,6 +623,7 @@ __device__ __noinline__ void elementwise_rows(uint32_t rc_addr, int64_t unit, ui
         const RowConst& rc = *reinterpret_cast<const RowConst*>(smem_raw + (rc_addr - smem_u32(smem_raw)));
         a.in = rc.in, a.in_stride = rc.in_stride, a.out = rc.out, a.out_stride = rc.out_stride;
         a.src_index = rc.src_index, a.n = rc.n, a.shifts = rc.shifts, a.angles = rc.angles;
+        a.angle_index = rc.angle_index;
         a.kind = rc.kind, a.p_in = rc.p_in, a.p_out = rc.p_out;
     }
     constexpr uint32_t ROWB = G * 8;  // bytes of one triangle entry (all translations)
@@ -811,6 +814,7 @@ translate_mma_kernel(TranslateArgs<double> a, MmaTables mt, MmaPlan plan, int64_
         RowConst& rc = *reinterpret_cast<RowConst*>(smem_raw + (rc_addr - sm));
         rc.in = a.in, rc.in_stride = a.in_stride, rc.out = a.out, rc.out_stride = a.out_stride;
         rc.src_index = a.src_index, rc.n = a.n, rc.shifts = a.shifts, rc.angles = a.angles;
+        rc.angle_index = a.angle_index;
         rc.kind = a.kind, rc.p_in = a.p_in, rc.p_out = a.p_out, rc.pad = 0;
     }
 

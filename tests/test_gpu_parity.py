@@ -350,6 +350,29 @@ def test_accumulation_many_ragged_targets_and_long_targets(oracle, h64, h32):
             assert bits_equal(got, want), (p, len(counts))
 
 
+def test_plan_geometry_per_distinct_shift(oracle, h64):
+    """The plan decomposes every DISTINCT shift once (hash table on the device) and falls
+    back to one entry per lane when the list has more distinct shifts than the table holds:
+    a list of 100 000 pairs over five shifts (signed zeros distinguish two of them), and one of
+    80 000 distinct shifts, both bit-exact."""
+    rng = np.random.default_rng(977)
+    ns, p = 40, 3
+    src = random_solids(rng, ns, p)
+    few = np.array([[0, 0, 1.5], [0.0, -0.0, 1.5], [1, 2, 3], [-2, 0.5, 0.25], [3, 0, 0]])
+    for sh in (few[rng.integers(0, 5, 100_000)], random_shifts(rng, 80_000, with_axes=False)):
+        counts = rng.integers(0, 400, 2000)
+        counts[-1] += len(sh) - counts.sum() if counts.sum() < len(sh) else 0
+        tgt_ptr = np.minimum(np.concatenate([[0], np.cumsum(counts)]), len(sh)).astype(np.int64)
+        tgt_ptr[-1] = len(sh)
+        idx = rng.integers(0, ns, len(sh)).astype(np.int32)
+        plan = h64.plan(tgt_ptr, idx, sh, ns)
+        got = plan.accumulate_host(p, p, src)
+        plan.close()
+        _, per_pair = oracle.translate("m2l", p, p, src[idx], sh)
+        want = sharding.accumulation_tree(per_pair, tgt_ptr, h64.accumulation_unit(p, p))
+        assert bits_equal(got, want)
+
+
 # ---- API contracts ---------------------------------------------------------
 
 def test_error_contracts(h64):
