@@ -133,6 +133,35 @@ int64_t sfmm_rows_len(int p);
 sfmm_status sfmm_pack_rows(sfmm_handle* h, int64_t n, int p, const void* d_aos,
                            void* d_rows, void* stream);
 
+/* ---- particle <-> expansion steps (the callers either side of the translation path) ----
+ * P2M replaces `mpole::p2m` (reference core/src/harmonics.cpp:105-117, core/include/mpole/
+ * harmonics.hpp:36-39) for a batch of boxes: box b owns the charges box_ptr[b] .. box_ptr[b+1]
+ * of `charges` ([n][4] = x y z q, the reference's point_charge) and has centre centers[b][3];
+ * its multipole of order `order` is written in `layout`:
+ *   SFMM_LAYOUT_AOS   [box][P(P+1)], the reference's solid layout (solid.hpp:59-70)
+ *   SFMM_LAYOUT_SOA   [c][out_stride], the input layout of sfmm_translate_soa / sfmm_m2l_accumulate
+ *   SFMM_LAYOUT_ROWS  [box][sfmm_rows_len(P)], the source layout of sfmm_m2l_accumulate_rows
+ * L2P replaces `mpole::eval_local` (harmonics.cpp:119-152, harmonics.hpp:48-51): out[i] is the
+ * potential of the local expansion of box point_box[i] (NULL: box i) at points[i][3].
+ * Results equal the reference's (parity build, -mfma -ffp-contract=fast) bit for bit, charges and
+ * sums taken in the reference's order. Device entry points take device pointers and a stream;
+ * the _host forms take host arrays (expansions in the AoS layout). Orders up to
+ * sfmm_harmonics_max_order() (32). */
+enum { SFMM_LAYOUT_SOA = 0, SFMM_LAYOUT_ROWS = 1, SFMM_LAYOUT_AOS = 2 };
+int sfmm_harmonics_max_order(void);
+sfmm_status sfmm_p2m(sfmm_handle* h, int64_t n_boxes, const int64_t* d_box_ptr,
+                     const void* d_charges, const void* d_centers, int order, int layout,
+                     void* d_out, int64_t out_stride, void* stream);
+sfmm_status sfmm_eval_local(sfmm_handle* h, int64_t n_points, const int32_t* d_point_box,
+                            const void* d_points, const void* d_centers, int64_t n_boxes,
+                            int order, int layout, const void* d_locals, int64_t stride,
+                            void* d_out, void* stream);
+sfmm_status sfmm_p2m_host(sfmm_handle* h, int64_t n_boxes, const int64_t* box_ptr,
+                          const void* charges, const void* centers, int order, void* out_aos);
+sfmm_status sfmm_eval_local_host(sfmm_handle* h, int64_t n_points, const int32_t* point_box,
+                                 const void* points, const void* centers, int64_t n_boxes,
+                                 int order, const void* locals_aos, void* out);
+
 /* ---- target-owned M2L accumulation (a full interaction-list level) -------
  * L[t] = sum over the sources s of target t of m2l(M[s], shift(t, s)), each
  * term computed exactly as the batched call computes it, summed without

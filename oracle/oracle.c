@@ -253,6 +253,81 @@ double orc_eval_local_f64(int order, const double* l, const double* center,
     return total;
 }
 
+/* ---- the same three functions in the arithmetic of the PARITY build ----------------------
+ * (reference compiled with -O2 -mavx2 -mfma -ffp-contract=fast, oracle/Makefile): the fused
+ * multiply-adds GCC forms in harmonics.cpp:18-50, 105-117, 119-152 written out explicitly
+ * (read off the object code of _ref/libmpole_ref.so; pinned bit for bit against it in
+ * tests/test_oracle.py). The CUDA P2M / L2P kernels (csrc/sfmm_harmonics.cu) are checked
+ * against these. norm(r) (solid.hpp:21-23) only feeds the zero test. */
+#define HARM_FMA_IMPL(SUF, REAL, FMA, SQRT, FABS, FMAX, RMIN)                                   \
+    static int harm_zero_##SUF(REAL x, REAL y, REAL z) {                                        \
+        const REAL ax = FABS(x), ay = FABS(y), az = FABS(z);                                    \
+        const REAL a = FMAX(FMAX(ax, ay), az);                                                  \
+        if (a == 0) return 1;                                                                   \
+        const REAL xs = ax / a, ys = ay / a, zs = az / a;                                       \
+        return a * SQRT(FMA(zs, zs, FMA(xs, xs, ys * ys))) < RMIN;                              \
+    }                                                                                           \
+    void orc_regular_fma_##SUF(int order, const REAL* r, REAL* out) {                           \
+        memset(out, 0, sizeof(REAL) * order * (order + 1));                                     \
+        out[0] = 1;                                                                             \
+        if (order == 1) return;                                                                 \
+        const REAL x = r[0], y = r[1], z = r[2];                                                \
+        if (harm_zero_##SUF(x, y, z)) return;                                                   \
+        const REAL r2 = FMA(z, z, FMA(x, x, y * y));                                            \
+        for (int n = 1; n < order; ++n) {                                                       \
+            const REAL inv2n = (REAL)1 / (REAL)(2 * n);                                         \
+            const REAL pre = out[(n - 1) * n + 2 * (n - 1)], pim = out[(n - 1) * n + 2 * (n - 1) + 1]; \
+            out[n * (n + 1) + 2 * n] = inv2n * FMA(-y, pim, x * pre);                           \
+            out[n * (n + 1) + 2 * n + 1] = inv2n * FMA(x, pim, y * pre);                        \
+            const REAL zf = (REAL)(2 * n - 1) * z;                                              \
+            for (int m = 0; m < n; ++m) {                                                       \
+                const REAL denom = (REAL)1 / (REAL)(n * n - m * m);                             \
+                REAL re = zf * out[(n - 1) * n + 2 * m], im = zf * out[(n - 1) * n + 2 * m + 1]; \
+                if (n - 2 >= m) {                                                               \
+                    re = FMA(-r2, out[(n - 2) * (n - 1) + 2 * m], re);                          \
+                    im = FMA(-r2, out[(n - 2) * (n - 1) + 2 * m + 1], im);                      \
+                }                                                                               \
+                out[n * (n + 1) + 2 * m] = denom * re;                                          \
+                out[n * (n + 1) + 2 * m + 1] = (m == 0) ? 0 : denom * im;                       \
+            }                                                                                   \
+        }                                                                                       \
+    }                                                                                           \
+    void orc_p2m_fma_##SUF(int count, const REAL* charges, const REAL* center, int order,       \
+                           REAL* out) {                                                         \
+        const int sz = order * (order + 1);                                                     \
+        REAL* rv = (REAL*)malloc(sizeof(REAL) * sz);                                            \
+        memset(out, 0, sizeof(REAL) * sz);                                                      \
+        for (int j = 0; j < count; ++j) {                                                       \
+            const REAL d[3] = {charges[4 * j] - center[0], charges[4 * j + 1] - center[1],      \
+                               charges[4 * j + 2] - center[2]};                                 \
+            orc_regular_fma_##SUF(order, d, rv);                                                \
+            const REAL q = charges[4 * j + 3];                                                  \
+            for (int i = 0; i < sz; ++i) out[i] = FMA(q, rv[i], out[i]);                        \
+        }                                                                                       \
+        free(rv);                                                                               \
+    }                                                                                           \
+    REAL orc_eval_local_fma_##SUF(int order, const REAL* l, const REAL* center, const REAL* x) { \
+        const int sz = order * (order + 1);                                                     \
+        REAL* rv = (REAL*)malloc(sizeof(REAL) * sz);                                            \
+        const REAL d[3] = {x[0] - center[0], x[1] - center[1], x[2] - center[2]};               \
+        orc_regular_fma_##SUF(order, d, rv);                                                    \
+        REAL total = 0;                                                                         \
+        for (int n = 0; n < order; ++n) {                                                       \
+            REAL row = 0;                                                                       \
+            for (int m = 1; m <= n; ++m) {                                                      \
+                const int i = n * (n + 1) + 2 * m;                                              \
+                row = row + FMA(l[i], rv[i], l[i + 1] * rv[i + 1]);                             \
+            }                                                                                   \
+            total = FMA(l[n * (n + 1)], rv[n * (n + 1)], total);                                \
+            total = total + (row + row);                                                        \
+        }                                                                                       \
+        free(rv);                                                                               \
+        return total;                                                                           \
+    }
+HARM_FMA_IMPL(f64, double, fma, sqrt, fabs, fmax, DBL_MIN)
+HARM_FMA_IMPL(f32, float, fmaf, sqrtf, fabsf, fmaxf, FLT_MIN)
+#undef HARM_FMA_IMPL
+
 /* pipeline.cpp:412-431 with solid::coeff (solid.hpp:110-116) for negative m:
  * L_n^m = (-1)^n sum_{k<P_in} sum_{|l|<=k} conj(M_k^l) S_{n+k}^{m+l}(r). */
 static void coeff(const double* s, int n, int m, double* re, double* im) {

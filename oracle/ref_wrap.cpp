@@ -234,6 +234,24 @@ double ref_eval_local_f64(int order, const double* l, const double* center,
                               {x[0], x[1], x[2]});
 }
 
+// single-precision forms of the three harmonics entry points
+void ref_p2m_f32(int count, const float* charges, const float* center, int order, float* out) {
+    std::vector<point_charge<float>> c(count);
+    for (int i = 0; i < count; ++i)
+        c[i] = {{charges[4 * i], charges[4 * i + 1], charges[4 * i + 2]}, charges[4 * i + 3]};
+    const auto m = p2m<float>(c, {center[0], center[1], center[2]}, order);
+    std::memcpy(out, m.data().data(), solid_size(order) * sizeof(float));
+}
+void ref_regular_f32(int order, const float* r, float* out) {
+    const auto s = regular<float>(order, {r[0], r[1], r[2]});
+    std::memcpy(out, s.data().data(), solid_size(order) * sizeof(float));
+}
+float ref_eval_local_f32(int order, const float* l, const float* center, const float* x) {
+    solid<float> s(solid_kind::local, order);
+    std::memcpy(s.data().data(), l, solid_size(order) * sizeof(float));
+    return eval_local<float>(s, {center[0], center[1], center[2]}, {x[0], x[1], x[2]});
+}
+
 // b: (2n+1)^2, f and g: (n+1)^2 each, all row-major double.
 void ref_swap_tables(int n, double* b, double* f, double* g) {
     const auto bb = wigner_b(n);

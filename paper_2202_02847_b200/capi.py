@@ -18,6 +18,7 @@ OK, INVALID_ARGUMENT, DOMAIN_ERROR, CUDA_ERROR, OUT_OF_MEMORY = range(5)
 M2L, M2M, L2L = 0, 1, 2
 F64, F32 = 0, 1
 SYNC_STATUS, ASYNC_STATUS = 0, 1
+LAYOUT_SOA, LAYOUT_ROWS, LAYOUT_AOS = 0, 1, 2
 
 KIND_BY_NAME = {"m2l": M2L, "m2m": M2M, "l2l": L2L}
 
@@ -57,6 +58,14 @@ _SIGNATURES = {
     "sfmm_m2l_level_host": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_int,
                                     c_int, c_void_p, c_void_p]),
     "sfmm_accumulation_unit": (c_int, [c_void_p, c_int, c_int]),
+    "sfmm_harmonics_max_order": (c_int, []),
+    "sfmm_p2m": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p,
+                         c_int64, c_void_p]),
+    "sfmm_eval_local": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_int,
+                                c_int, c_void_p, c_int64, c_void_p, c_void_p]),
+    "sfmm_p2m_host": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+    "sfmm_eval_local_host": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_int,
+                                     c_void_p, c_void_p]),
     "sfmm_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
     "sfmm_measure_fma_peak": (c_int, [c_void_p, POINTER(c_double)]),
     "sfmm_measure_dmma_peak": (c_int, [c_void_p, POINTER(c_double)]),
@@ -294,6 +303,48 @@ class Handle:
 
     def pack_rows(self, n: int, p: int, d_aos, d_rows, stream=None) -> None:
         check(self._lib.sfmm_pack_rows(self._h, n, p, _ptr(d_aos), _ptr(d_rows), _ptr(stream)))
+
+    # -- particle <-> expansion steps (reference harmonics.cpp: p2m, eval_local) --------
+    def p2m(self, n_boxes: int, d_box_ptr, d_charges, d_centers, order: int, layout: int, d_out,
+            out_stride: int = 0, stream=None) -> None:
+        check(self._lib.sfmm_p2m(self._h, n_boxes, _ptr(d_box_ptr), _ptr(d_charges), _ptr(d_centers),
+                                 order, layout, _ptr(d_out), out_stride, _ptr(stream)))
+
+    def eval_local(self, n_points: int, d_point_box, d_points, d_centers, n_boxes: int, order: int,
+                   layout: int, d_locals, stride: int, d_out, stream=None) -> None:
+        check(self._lib.sfmm_eval_local(self._h, n_points, _ptr(d_point_box), _ptr(d_points),
+                                        _ptr(d_centers), n_boxes, order, layout, _ptr(d_locals), stride,
+                                        _ptr(d_out), _ptr(stream)))
+
+    def p2m_host(self, box_ptr, charges, centers, order: int) -> np.ndarray:
+        """Multipoles [box][P(P+1)] of boxes owning charges[box_ptr[b]:box_ptr[b+1]] = (x, y, z, q)."""
+        box_ptr = np.ascontiguousarray(box_ptr, np.int64)
+        charges = np.ascontiguousarray(charges, self.dtype).reshape(-1, 4)
+        centers = np.ascontiguousarray(centers, self.dtype).reshape(-1, 3)
+        n_boxes = len(box_ptr) - 1
+        if len(centers) < n_boxes or (n_boxes > 0 and len(charges) < box_ptr[-1]):
+            raise InvalidArgument(INVALID_ARGUMENT, "charges / centers shorter than box_ptr says")
+        out = np.empty((n_boxes, solid_size(order)), self.dtype)
+        check(self._lib.sfmm_p2m_host(self._h, n_boxes, _ptr(box_ptr), _ptr(charges), _ptr(centers),
+                                      order, _ptr(out)))
+        return out
+
+    def eval_local_host(self, point_box, points, centers, order: int, locals_aos) -> np.ndarray:
+        """Potential of the local expansion of box point_box[i] (None: box i) at points[i]."""
+        points = np.ascontiguousarray(points, self.dtype).reshape(-1, 3)
+        centers = np.ascontiguousarray(centers, self.dtype).reshape(-1, 3)
+        locals_aos = np.ascontiguousarray(locals_aos, self.dtype)
+        n_boxes = len(centers)
+        if locals_aos.size < n_boxes * solid_size(order):
+            raise InvalidArgument(INVALID_ARGUMENT, "locals shorter than the boxes")
+        if point_box is not None:
+            point_box = np.ascontiguousarray(point_box, np.int32)
+            if len(point_box) < len(points):
+                raise InvalidArgument(INVALID_ARGUMENT, "point_box shorter than points")
+        out = np.empty(len(points), self.dtype)
+        check(self._lib.sfmm_eval_local_host(self._h, len(points), _ptr(point_box), _ptr(points),
+                                             _ptr(centers), n_boxes, order, _ptr(locals_aos), _ptr(out)))
+        return out
 
     # -- target-owned accumulation -----------------------------------------
     def plan(self, tgt_ptr, src_index, shifts, n_sources: int) -> "Plan":

@@ -1065,6 +1065,125 @@ sfmm_status sfmm_pack_soa(sfmm_handle* h, int64_t n, int p, const void* d_aos, v
 
 int64_t sfmm_rows_len(int p) { return p < 1 ? 0 : rows_off(p); }
 
+// ---- particle <-> expansion steps -----------------------------------------
+int sfmm_harmonics_max_order(void) { return harmonics_max_order(); }
+
+static bool harmonics_layout_ok(int layout) {
+    return layout == SFMM_LAYOUT_SOA || layout == SFMM_LAYOUT_ROWS || layout == SFMM_LAYOUT_AOS;
+}
+
+sfmm_status sfmm_p2m(sfmm_handle* h, int64_t n_boxes, const int64_t* d_box_ptr, const void* d_charges,
+                     const void* d_centers, int order, int layout, void* d_out, int64_t out_stride,
+                     void* stream) {
+    if (!h || n_boxes < 0 || !harmonics_layout_ok(layout))
+        return fail(SFMM_INVALID_ARGUMENT, "bad p2m arguments");
+    if (order < 1 || order > h->order) return fail(SFMM_INVALID_ARGUMENT, "order out of range for this handle");
+    if (order > harmonics_max_order())
+        return fail(SFMM_INVALID_ARGUMENT, "p2m / eval_local on the device cover orders <= 32");
+    if (n_boxes == 0) return SFMM_OK;
+    if (!d_box_ptr || !d_charges || !d_centers || !d_out) return fail(SFMM_INVALID_ARGUMENT, "null pointer");
+    if (layout == SFMM_LAYOUT_SOA && out_stride < n_boxes)
+        return fail(SFMM_INVALID_ARGUMENT, "stride smaller than the batch");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    h->launches += 1;
+    if (h->precision == SFMM_F64)
+        CU(launch_p2m<double>(d_box_ptr, (const double*)d_charges, (const double*)d_centers, n_boxes, order,
+                              layout, (double*)d_out, out_stride, s));
+    else
+        CU(launch_p2m<float>(d_box_ptr, (const float*)d_charges, (const float*)d_centers, n_boxes, order,
+                             layout, (float*)d_out, out_stride, s));
+    return SFMM_OK;
+}
+
+sfmm_status sfmm_eval_local(sfmm_handle* h, int64_t n_points, const int32_t* d_point_box,
+                            const void* d_points, const void* d_centers, int64_t n_boxes, int order,
+                            int layout, const void* d_locals, int64_t stride, void* d_out, void* stream) {
+    if (!h || n_points < 0 || n_boxes < 0 || !harmonics_layout_ok(layout))
+        return fail(SFMM_INVALID_ARGUMENT, "bad eval_local arguments");
+    if (order < 1 || order > h->order) return fail(SFMM_INVALID_ARGUMENT, "order out of range for this handle");
+    if (order > harmonics_max_order())
+        return fail(SFMM_INVALID_ARGUMENT, "p2m / eval_local on the device cover orders <= 32");
+    if (n_points == 0) return SFMM_OK;
+    if (!d_points || !d_centers || !d_locals || !d_out) return fail(SFMM_INVALID_ARGUMENT, "null pointer");
+    if (layout == SFMM_LAYOUT_SOA && stride < n_boxes)
+        return fail(SFMM_INVALID_ARGUMENT, "stride smaller than the batch");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    h->launches += 1;
+    if (h->precision == SFMM_F64)
+        CU(launch_eval_local<double>(d_point_box, (const double*)d_points, (const double*)d_centers, n_points,
+                                     n_boxes, order, layout, (const double*)d_locals, stride, (double*)d_out, s));
+    else
+        CU(launch_eval_local<float>(d_point_box, (const float*)d_points, (const float*)d_centers, n_points,
+                                    n_boxes, order, layout, (const float*)d_locals, stride, (float*)d_out, s));
+    return SFMM_OK;
+}
+
+// host-buffer forms (the reference's p2m / eval_local take host objects, harmonics.hpp:36-51)
+sfmm_status sfmm_p2m_host(sfmm_handle* h, int64_t n_boxes, const int64_t* box_ptr, const void* charges,
+                          const void* centers, int order, void* out_aos) {
+    if (!h || n_boxes < 0) return fail(SFMM_INVALID_ARGUMENT, "bad p2m arguments");
+    if (n_boxes == 0) return SFMM_OK;
+    if (!box_ptr || !centers || !out_aos) return fail(SFMM_INVALID_ARGUMENT, "null pointer");
+    for (int64_t b = 0; b < n_boxes; ++b)
+        if (box_ptr[b + 1] < box_ptr[b]) return fail(SFMM_INVALID_ARGUMENT, "box_ptr must be non-decreasing");
+    const int64_t nq = box_ptr[n_boxes] - box_ptr[0];
+    if (nq > 0 && !charges) return fail(SFMM_INVALID_ARGUMENT, "null pointer");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = host_stream(h->device);
+    const size_t es = h->precision == SFMM_F64 ? 8 : 4;
+    DevBuf d_ptr(s), d_q(s), d_c(s), d_out(s);
+    CU(d_ptr.alloc(sizeof(int64_t) * (n_boxes + 1)));
+    CU(d_q.alloc(es * 4 * std::max<int64_t>(nq, 1)));
+    CU(d_c.alloc(es * 3 * n_boxes));
+    CU(d_out.alloc(es * solid_len(order) * n_boxes));
+    std::vector<int64_t> rel((size_t)n_boxes + 1);
+    for (int64_t b = 0; b <= n_boxes; ++b) rel[(size_t)b] = box_ptr[b] - box_ptr[0];
+    CU(cudaMemcpyAsync(d_ptr.p, rel.data(), sizeof(int64_t) * (n_boxes + 1), cudaMemcpyHostToDevice, s));
+    if (nq > 0)
+        CU(cudaMemcpyAsync(d_q.p, (const char*)charges + es * 4 * box_ptr[0], es * 4 * nq, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d_c.p, centers, es * 3 * n_boxes, cudaMemcpyHostToDevice, s));
+    const sfmm_status st = sfmm_p2m(h, n_boxes, d_ptr.as<int64_t>(), d_q.p, d_c.p, order, SFMM_LAYOUT_AOS,
+                                    d_out.p, 0, s);
+    if (st != SFMM_OK) return st;
+    CU(cudaMemcpyAsync(out_aos, d_out.p, es * solid_len(order) * n_boxes, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    return SFMM_OK;
+}
+
+sfmm_status sfmm_eval_local_host(sfmm_handle* h, int64_t n_points, const int32_t* point_box,
+                                 const void* points, const void* centers, int64_t n_boxes, int order,
+                                 const void* locals_aos, void* out) {
+    if (!h || n_points < 0 || n_boxes < 0) return fail(SFMM_INVALID_ARGUMENT, "bad eval_local arguments");
+    if (n_points == 0) return SFMM_OK;
+    if (!points || !centers || !locals_aos || !out) return fail(SFMM_INVALID_ARGUMENT, "null pointer");
+    if (!point_box && n_boxes < n_points) return fail(SFMM_INVALID_ARGUMENT, "one box per point expected");
+    if (point_box)
+        for (int64_t i = 0; i < n_points; ++i)
+            if (point_box[i] < 0 || point_box[i] >= n_boxes)
+                return fail(SFMM_INVALID_ARGUMENT, "box index out of range");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = host_stream(h->device);
+    const size_t es = h->precision == SFMM_F64 ? 8 : 4;
+    DevBuf d_pb(s), d_x(s), d_c(s), d_l(s), d_out(s);
+    CU(d_pb.alloc(sizeof(int32_t) * n_points));
+    CU(d_x.alloc(es * 3 * n_points));
+    CU(d_c.alloc(es * 3 * n_boxes));
+    CU(d_l.alloc(es * solid_len(order) * n_boxes));
+    CU(d_out.alloc(es * n_points));
+    if (point_box) CU(cudaMemcpyAsync(d_pb.p, point_box, sizeof(int32_t) * n_points, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d_x.p, points, es * 3 * n_points, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d_c.p, centers, es * 3 * n_boxes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d_l.p, locals_aos, es * solid_len(order) * n_boxes, cudaMemcpyHostToDevice, s));
+    const sfmm_status st = sfmm_eval_local(h, n_points, point_box ? d_pb.as<int32_t>() : nullptr, d_x.p, d_c.p,
+                                           n_boxes, order, SFMM_LAYOUT_AOS, d_l.p, 0, d_out.p, s);
+    if (st != SFMM_OK) return st;
+    CU(cudaMemcpyAsync(out, d_out.p, es * n_points, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    return SFMM_OK;
+}
+
 sfmm_status sfmm_pack_rows(sfmm_handle* h, int64_t n, int p, const void* d_aos, void* d_rows,
                            void* stream) {
     if (!h || !d_aos || !d_rows || p < 1 || n < 0)

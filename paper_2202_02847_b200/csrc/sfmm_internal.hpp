@@ -157,4 +157,20 @@ cudaError_t launch_reduce_groups(const Real* partial, int64_t n_groups, const in
                                  int per, int64_t n_targets, int p_out, Real* out,
                                  int64_t out_stride, cudaStream_t stream);
 
+// ---- particle <-> expansion steps (sfmm_harmonics.cu; reference harmonics.cpp) ----------------
+// layout of the expansions: LAYOUT_SOA, LAYOUT_ROWS or LAYOUT_AOS ([box][P(P+1)], solid.hpp:59-70)
+enum : int { LAYOUT_AOS = 2 };
+int harmonics_max_order();
+// P2M (harmonics.cpp:105-117): charges [n][4] = x y z q, box b owns charges box_ptr[b] .. box_ptr[b+1]
+template <typename Real>
+cudaError_t launch_p2m(const int64_t* box_ptr, const Real* charges, const Real* centers,
+                       int64_t n_boxes, int order, int layout, Real* out, int64_t stride,
+                       cudaStream_t stream);
+// L2P (harmonics.cpp:119-152): out[i] = eval_local(L[point_box[i]], centre, points[i]);
+// point_box == nullptr: point i belongs to box i
+template <typename Real>
+cudaError_t launch_eval_local(const int32_t* point_box, const Real* points, const Real* centers,
+                              int64_t n_points, int64_t n_boxes, int order, int layout,
+                              const Real* locals, int64_t stride, Real* out, cudaStream_t stream);
+
 }  // namespace sfmm

@@ -63,6 +63,8 @@ class Oracle(_Base):
     def __init__(self):
         self.lib = ctypes.CDLL(str(build_oracle()))
         self.lib.orc_eval_local_f64.restype = c_double
+        self.lib.orc_eval_local_fma_f64.restype = c_double
+        self.lib.orc_eval_local_fma_f32.restype = ctypes.c_float
         self.lib.orc_normalized_error_f64.restype = c_double
 
     def _translate(self, kind, p_in, p_out, src, shifts, dtype):
@@ -109,6 +111,27 @@ class Oracle(_Base):
         out = np.zeros(solid_size(order))
         self.lib.orc_regular_f64(c_int(order), _p(r), _p(out))
         return out
+
+    # the same functions in the arithmetic of the parity build (explicit fused multiply-adds)
+    def regular_fma(self, order, r, dtype=np.float64):
+        r = np.ascontiguousarray(r, dtype)
+        out = np.zeros(solid_size(order), dtype)
+        fn = self.lib.orc_regular_fma_f64 if dtype == np.float64 else self.lib.orc_regular_fma_f32
+        fn(c_int(order), _p(r), _p(out))
+        return out
+
+    def p2m_fma(self, charges, center, order, dtype=np.float64):
+        charges = np.ascontiguousarray(charges, dtype).reshape(-1, 4)
+        center = np.ascontiguousarray(center, dtype)
+        out = np.zeros(solid_size(order), dtype)
+        fn = self.lib.orc_p2m_fma_f64 if dtype == np.float64 else self.lib.orc_p2m_fma_f32
+        fn(c_int(len(charges)), _p(charges), _p(center), c_int(order), _p(out))
+        return out
+
+    def eval_local_fma(self, order, l, center, x, dtype=np.float64):
+        fn = self.lib.orc_eval_local_fma_f64 if dtype == np.float64 else self.lib.orc_eval_local_fma_f32
+        return dtype(fn(c_int(order), _p(np.ascontiguousarray(l, dtype)),
+                        _p(np.ascontiguousarray(center, dtype)), _p(np.ascontiguousarray(x, dtype))))
 
     def singular(self, order, r):
         r = np.ascontiguousarray(r, np.float64)
@@ -159,6 +182,8 @@ class Reference(_Base):
     def __init__(self, path: Path):
         self.lib = ctypes.CDLL(str(path))
         self.lib.ref_eval_local_f64.restype = c_double
+        if hasattr(self.lib, "ref_eval_local_f32"):
+            self.lib.ref_eval_local_f32.restype = ctypes.c_float
         self.path = path
 
     @classmethod
@@ -207,16 +232,18 @@ class Reference(_Base):
                                         _p(out))
         return st, out
 
-    def p2m(self, charges, center, order):
-        charges = np.ascontiguousarray(charges, np.float64).reshape(-1, 4)
-        center = np.ascontiguousarray(center, np.float64)
-        out = np.zeros(solid_size(order))
-        self.lib.ref_p2m_f64(c_int(len(charges)), _p(charges), _p(center), c_int(order), _p(out))
+    def p2m(self, charges, center, order, dtype=np.float64):
+        charges = np.ascontiguousarray(charges, dtype).reshape(-1, 4)
+        center = np.ascontiguousarray(center, dtype)
+        out = np.zeros(solid_size(order), dtype)
+        fn = self.lib.ref_p2m_f64 if dtype == np.float64 else self.lib.ref_p2m_f32
+        fn(c_int(len(charges)), _p(charges), _p(center), c_int(order), _p(out))
         return out
 
-    def regular(self, order, r):
-        out = np.zeros(solid_size(order))
-        self.lib.ref_regular_f64(c_int(order), _p(np.ascontiguousarray(r, np.float64)), _p(out))
+    def regular(self, order, r, dtype=np.float64):
+        out = np.zeros(solid_size(order), dtype)
+        fn = self.lib.ref_regular_f64 if dtype == np.float64 else self.lib.ref_regular_f32
+        fn(c_int(order), _p(np.ascontiguousarray(r, dtype)), _p(out))
         return out
 
     def singular(self, order, r):
@@ -225,10 +252,10 @@ class Reference(_Base):
                                        _p(out))
         return st, out
 
-    def eval_local(self, order, l, center, x):
-        return self.lib.ref_eval_local_f64(c_int(order), _p(np.ascontiguousarray(l, np.float64)),
-                                           _p(np.ascontiguousarray(center, np.float64)),
-                                           _p(np.ascontiguousarray(x, np.float64)))
+    def eval_local(self, order, l, center, x, dtype=np.float64):
+        fn = self.lib.ref_eval_local_f64 if dtype == np.float64 else self.lib.ref_eval_local_f32
+        return dtype(fn(c_int(order), _p(np.ascontiguousarray(l, dtype)),
+                        _p(np.ascontiguousarray(center, dtype)), _p(np.ascontiguousarray(x, dtype))))
 
     def swap_tables(self, n):
         b = np.zeros((2 * n + 1, 2 * n + 1))

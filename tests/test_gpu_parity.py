@@ -373,6 +373,91 @@ def test_plan_geometry_per_distinct_shift(oracle, h64):
         assert bits_equal(got, want)
 
 
+# ---- particle <-> expansion steps --------------------------
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_p2m_and_eval_local_bit_exact(oracle, h64, h32, prec):
+    """Device P2M and L2P (harmonics.cpp:105-152) against the parity-build restatement
+    (oracle.p2m_fma / eval_local_fma, pinned to the compiled reference in test_oracle.py):
+    ragged boxes incl. empty ones, a charge at the centre (zero argument), orders 1..max."""
+    h, dt, pmax = (h64, np.float64, 30) if prec == "f64" else (h32, np.float32, 18)
+    rng = np.random.default_rng(409)
+    for p in (1, 2, 5, 9, 16, 17, pmax):
+        counts = np.concatenate([[0, 1, 33], rng.integers(0, 40, 20)])
+        box_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        nb = len(counts)
+        centers = rng.standard_normal((nb, 3)).astype(dt)
+        ch = np.empty((int(box_ptr[-1]), 4), dt)
+        for b in range(nb):
+            lo, hi = box_ptr[b], box_ptr[b + 1]
+            ch[lo:hi, :3] = centers[b] + (rng.random((hi - lo, 3)) - 0.5).astype(dt)
+            ch[lo:hi, 3] = rng.choice([-1.0, 1.0], hi - lo)
+        ch[box_ptr[2], :3] = centers[2]            # a charge at the centre of its box
+        got = h.p2m_host(box_ptr, ch, centers, p)
+        want = np.stack([oracle.p2m_fma(ch[box_ptr[b]:box_ptr[b + 1]], centers[b], p, dt) for b in range(nb)])
+        assert bits_equal(got, want), (prec, p)
+        # L2P: the multipoles stand in for local expansions (any coefficients do)
+        npts = 57
+        pb = rng.integers(0, nb, npts).astype(np.int32)
+        x = (centers[pb] + (rng.random((npts, 3)) - 0.5).astype(dt) * dt(0.8)).astype(dt)
+        x[0] = centers[pb[0]]
+        phi = h.eval_local_host(pb, x, centers, p, want)
+        ref_phi = np.array([oracle.eval_local_fma(p, want[pb[i]], centers[pb[i]], x[i], dt) for i in range(npts)], dt)
+        assert bits_equal(phi, ref_phi), (prec, p)
+
+
+@pytest.mark.gpu
+def test_p2m_layouts_feed_the_translation_path(oracle, h64):
+    """P2M written directly in the SoA and rows layouts, then M2L and L2P on the device: the
+    device pipeline P2M -> M2L -> L2P equals the oracle pipeline bit for bit and approximates the
+    direct potential (harmonics.cpp:87-103) as the truncation allows."""
+    import torch
+    rng = np.random.default_rng(411)
+    p, nb, per = 12, 200, 16
+    dev = torch.device("cuda", 0)
+    centers = (rng.random((nb, 3)) * 4).astype(np.float64)
+    ch = np.empty((nb * per, 4))
+    ch[:, :3] = np.repeat(centers, per, 0) + (rng.random((nb * per, 3)) - 0.5)
+    ch[:, 3] = rng.standard_normal(nb * per)
+    box_ptr = np.arange(0, nb * per + 1, per, dtype=np.int64)
+    d_ptr, d_ch, d_c = (torch.from_numpy(a).to(dev) for a in (box_ptr, ch, centers))
+    S = solid_size(p)
+    stride = 256
+    d_soa = torch.zeros((S, stride), dtype=torch.float64, device=dev)
+    d_rows = torch.full((nb, h64.rows_len(p)), 7.0, dtype=torch.float64, device=dev)
+    d_aos = torch.zeros((nb, S), dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    for layout, buf, stride_arg in ((capi.LAYOUT_SOA, d_soa, stride), (capi.LAYOUT_ROWS, d_rows, 0), (capi.LAYOUT_AOS, d_aos, 0)):
+        h64.p2m(nb, d_ptr.data_ptr(), d_ch.data_ptr(), d_c.data_ptr(), p, layout, buf.data_ptr(), stride_arg, st)
+    torch.cuda.synchronize()
+    want = np.stack([oracle.p2m_fma(ch[b * per:(b + 1) * per], centers[b], p) for b in range(nb)])
+    assert bits_equal(d_aos.cpu().numpy(), want)
+    assert bits_equal(d_soa.cpu().numpy()[:, :nb].T, want)
+    d_rows_ref = torch.empty_like(d_rows)
+    h64.pack_rows(nb, p, d_aos.data_ptr(), d_rows_ref.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(d_rows, d_rows_ref)
+    # M2L of every multipole to a far centre, then L2P there
+    sh = np.tile([6.0, 5.0, 7.0], (nb, 1)) + rng.random((nb, 3))
+    d_sh = torch.from_numpy(sh).to(dev)
+    d_loc = torch.zeros((S, stride), dtype=torch.float64, device=dev)
+    h64.translate_soa(capi.M2L, nb, p, p, d_soa.data_ptr(), stride, d_sh.data_ptr(), d_loc.data_ptr(), stride, st)
+    lc = centers + sh
+    x = lc + (rng.random((nb, 3)) - 0.5) * 0.5
+    d_lc, d_x = torch.from_numpy(lc).to(dev), torch.from_numpy(x).to(dev)
+    d_phi = torch.empty(nb, dtype=torch.float64, device=dev)
+    h64.eval_local(nb, None, d_x.data_ptr(), d_lc.data_ptr(), nb, p, capi.LAYOUT_SOA, d_loc.data_ptr(), stride,
+                   d_phi.data_ptr(), st)
+    torch.cuda.synchronize()
+    loc = oracle.translate("m2l", p, p, want, sh)[1]
+    phi = np.array([oracle.eval_local_fma(p, loc[b], lc[b], x[b]) for b in range(nb)])
+    assert bits_equal(d_phi.cpu().numpy(), phi)
+    direct = np.array([np.sum(ch[b * per:(b + 1) * per, 3] /
+                              np.linalg.norm(x[b] - ch[b * per:(b + 1) * per, :3], axis=1)) for b in range(nb)])
+    assert np.max(np.abs(phi - direct)) < 1e-6 * np.max(np.abs(direct))
+
+
 # ---- API contracts ---------------------------------------------------------
 
 def test_error_contracts(h64):

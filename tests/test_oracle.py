@@ -287,6 +287,36 @@ def test_oracle_aux_functions_match_reference(oracle, ref):
     assert normalized_error(oracle.m2l_naive(9, 7, m, sh)[1], ref.m2l_naive(9, 7, m, sh)[1]) < 1e-14
 
 
+def test_harmonics_fma_restatement_is_the_parity_build_bit_for_bit(oracle, ref):
+    """regular / p2m / eval_local with the fused multiply-adds of the parity build written out
+    (oracle.c HARM_FMA_IMPL) against the compiled reference (harmonics.cpp:18-50, 105-152),
+    double and single precision, including the zero / subnormal argument (R_0^0 only) and the
+    known answers R_1^1(1,2,3) = 0.5 + 1.0i, R_n^0(0,0,1) = 1/n! (test_harmonics.cpp:21-71)."""
+    rng = np.random.default_rng(23)
+    for dt, pmax in ((np.float64, 30), (np.float32, 18)):
+        for trial in range(40):
+            p = int(rng.integers(1, pmax + 1))
+            r = (rng.standard_normal(3) * rng.choice([1e-3, 0.3, 1.0, 4.0])).astype(dt)
+            if trial == 0: r[:] = 0
+            if trial == 1: r[:] = [0, 0, 1e-310 if dt == np.float64 else 1e-40]
+            if trial == 2: r[:] = [0, 0, 1.5]
+            assert bits_equal(oracle.regular_fma(p, r, dt), ref.regular(p, r, dt)), (dt, p, r)
+            ch = rng.standard_normal((int(rng.integers(0, 40)), 4)).astype(dt)
+            c = rng.standard_normal(3).astype(dt) * dt(0.1)
+            assert bits_equal(oracle.p2m_fma(ch, c, p, dt), ref.p2m(ch, c, p, dt)), (dt, p)
+            l = random_solids(rng, 1, p, dt)[0]
+            x = c + r
+            a, b = oracle.eval_local_fma(p, l, c, x, dt), ref.eval_local(p, l, c, x, dt)
+            assert a == b or (np.isnan(a) and np.isnan(b)), (dt, p, a, b)
+    r11 = oracle.regular_fma(3, [1.0, 2.0, 3.0])
+    assert r11[1 * 2 + 2] == 0.5 and r11[1 * 2 + 3] == 1.0
+    rz = oracle.regular_fma(8, [0.0, 0.0, 1.0])
+    fact = 1.0
+    for n in range(8):
+        fact *= max(n, 1)
+        assert rz[n * (n + 1)] == pytest.approx(1.0 / fact, rel=1e-15)
+
+
 def test_reference_error_codes_match_oracle(oracle, ref):
     rng = np.random.default_rng(13)
     m = random_solids(rng, 2, 6)
