@@ -8,6 +8,8 @@
 //   operator_data (order, max_order, acquire)                include/mpole/operators.hpp:57-95
 //   workspace                                                include/mpole/workspace.hpp:18-51
 //   m2l / m2m / l2l, batched and single-request              include/mpole/pipeline.hpp:30-56
+//   point_charge, p2m, eval_local (device P2M / L2P)         include/mpole/harmonics.hpp:10-51
+//   write_solid / read_solid(s) / read_charges / write_charges   include/mpole/io.hpp:12-34
 //
 // Differences that follow from running on a device: operator_data owns the
 // device handle (tables + scratch), so `workspace` is a plain tag object kept
@@ -24,10 +26,14 @@
 #include <complex>
 #include <cstddef>
 #include <cstdint>
+#include <istream>
 #include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
+#include <optional>
+#include <ostream>
+#include <sstream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -287,6 +293,209 @@ solid<Real> l2l(const operator_data<Real>& ops, const solid<Real>& l, const vec3
     translation_request<Real> req{&l, shift, target_order, &out};
     l2l<Real>(ops, std::span<const translation_request<Real>>(&req, 1), ws);
     return out;
+}
+
+// ---- particle <-> expansion steps on the device (harmonics.hpp:10-51) ----------------------
+// The reference's p2m / eval_local are free functions without a handle; here the device
+// handle travels in `ops`. Batched forms (one call for many boxes / points) come first, the
+// reference's single-object signatures forward to them.
+template <typename Real>
+struct point_charge {
+    vec3<Real> position;
+    Real charge;
+};
+
+/// Multipoles of `centers.size()` boxes; box b owns charges[box_ptr[b] .. box_ptr[b+1]).
+template <typename Real>
+std::vector<solid<Real>> p2m(const operator_data<Real>& ops, std::span<const point_charge<Real>> charges,
+                             std::span<const std::int64_t> box_ptr, std::span<const vec3<Real>> centers, int order) {
+    static_assert(sizeof(point_charge<Real>) == 4 * sizeof(Real) && sizeof(vec3<Real>) == 3 * sizeof(Real));
+    if (order < 1 || order > ops.order()) throw std::invalid_argument("order out of range for this operator_data");
+    if (box_ptr.size() != centers.size() + 1) throw std::invalid_argument("box_ptr must have one entry per box plus one");
+    const std::size_t nb = centers.size();
+    std::vector<Real> flat(nb * solid_size(order));
+    detail::raise(sfmm_p2m_host(ops.handle(), static_cast<int64_t>(nb), box_ptr.data(), charges.data(), centers.data(),
+                                order, flat.data()));
+    std::vector<solid<Real>> out;
+    out.reserve(nb);
+    for (std::size_t b = 0; b < nb; ++b) {
+        out.emplace_back(solid_kind::multipole, order);
+        std::copy_n(flat.begin() + b * solid_size(order), solid_size(order), out.back().data().begin());
+    }
+    return out;
+}
+template <typename Real>
+solid<Real> p2m(const operator_data<Real>& ops, std::span<const point_charge<Real>> sources,
+                const vec3<Real>& center, int order) {
+    const std::int64_t ptr[2] = {0, static_cast<std::int64_t>(sources.size())};
+    return std::move(p2m<Real>(ops, sources, std::span<const std::int64_t>(ptr, 2),
+                               std::span<const vec3<Real>>(&center, 1), order)[0]);
+}
+
+/// Potentials of local expansions: point i is evaluated with locals[box[i]] about centers[box[i]].
+template <typename Real>
+std::vector<Real> eval_local(const operator_data<Real>& ops, std::span<const solid<Real>> locals,
+                             std::span<const vec3<Real>> centers, std::span<const std::int32_t> box,
+                             std::span<const vec3<Real>> points) {
+    if (locals.empty() || locals.size() != centers.size() || box.size() != points.size())
+        throw std::invalid_argument("eval_local: array sizes do not match");
+    const int order = locals[0].order();
+    if (order > ops.order()) throw std::invalid_argument("order out of range for this operator_data");
+    std::vector<Real> flat(locals.size() * solid_size(order));
+    for (std::size_t b = 0; b < locals.size(); ++b) {
+        if (locals[b].order() != order) throw std::invalid_argument("eval_local: one order per call");
+        std::copy(locals[b].data().begin(), locals[b].data().end(), flat.begin() + b * solid_size(order));
+    }
+    std::vector<Real> out(points.size());
+    detail::raise(sfmm_eval_local_host(ops.handle(), static_cast<int64_t>(points.size()), box.data(), points.data(),
+                                       centers.data(), static_cast<int64_t>(locals.size()), order, flat.data(),
+                                       out.data()));
+    return out;
+}
+template <typename Real>
+Real eval_local(const operator_data<Real>& ops, const solid<Real>& l, const vec3<Real>& center, const vec3<Real>& x) {
+    const std::int32_t zero = 0;
+    return eval_local<Real>(ops, std::span<const solid<Real>>(&l, 1), std::span<const vec3<Real>>(&center, 1),
+                            std::span<const std::int32_t>(&zero, 1), std::span<const vec3<Real>>(&x, 1))[0];
+}
+
+// ---- text format of the reference tool (io.hpp:12-34, io.cpp:68-159) -----------------------
+// `SOLID <kind letter> <P>` then P(P+1) reals in storage order, one row of the triangle per
+// line, max_digits10 significant digits: files written here read back bit for bit, and files
+// of the reference's `mpole` tool are accepted (and vice versa). Charges: one `x y z q` per
+// line, blank lines and lines starting with '#' skipped. Malformed input raises
+// std::runtime_error naming the line.
+inline char kind_letter(solid_kind k) {
+    switch (k) {
+        case solid_kind::multipole: return 'M';
+        case solid_kind::local: return 'L';
+        case solid_kind::regular: return 'R';
+        default: return 'S';
+    }
+}
+inline solid_kind kind_from_letter(char c) {
+    switch (c) {
+        case 'M': return solid_kind::multipole;
+        case 'L': return solid_kind::local;
+        case 'R': return solid_kind::regular;
+        case 'S': return solid_kind::singular;
+        default: throw std::invalid_argument(std::string("unknown solid kind '") + c + "'");
+    }
+}
+
+template <typename Real>
+void write_solid(std::ostream& os, const solid<Real>& s) {
+    os << "SOLID " << kind_letter(s.kind()) << ' ' << s.order() << '\n';
+    os.precision(std::numeric_limits<Real>::max_digits10);
+    for (int n = 0; n < s.order(); ++n) {
+        for (int m = 0; m <= n; ++m) os << (m ? " " : "") << s.re(n, m) << ' ' << s.im(n, m);
+        os << '\n';
+    }
+}
+
+namespace detail {
+// whitespace-separated tokens with the number of the line they were found on
+struct token_stream {
+    std::istream& is;
+    std::istringstream cur;
+    int line_no = 0;
+    explicit token_stream(std::istream& in) : is(in) {}
+    bool next(std::string& tok) {
+        while (!(cur >> tok)) {
+            std::string line;
+            if (!std::getline(is, line)) return false;
+            ++line_no;
+            cur.clear();
+            cur.str(line);
+        }
+        return true;
+    }
+    [[noreturn]] void fail(const std::string& what) const {
+        throw std::runtime_error("line " + std::to_string(line_no) + ": " + what);
+    }
+};
+}  // namespace detail
+
+template <typename Real>
+std::optional<solid<Real>> read_solid(std::istream& is) {
+    detail::token_stream ts(is);
+    std::string tok;
+    if (!ts.next(tok)) return std::nullopt;
+    if (tok != "SOLID") ts.fail("expected 'SOLID' header, got '" + tok + "'");
+    if (!ts.next(tok) || tok.size() != 1) ts.fail("expected solid kind M, L, R or S");
+    solid_kind kind;
+    try {
+        kind = kind_from_letter(tok[0]);
+    } catch (const std::invalid_argument&) {
+        ts.fail("expected solid kind M, L, R or S, got '" + tok + "'");
+    }
+    int order = 0;
+    {
+        std::string ot;
+        std::size_t used = 0;
+        const bool have = ts.next(ot);
+        try {
+            if (!have) throw std::invalid_argument("");
+            order = std::stoi(ot, &used);
+            if (used != ot.size()) throw std::invalid_argument(ot);
+        } catch (const std::exception&) {
+            ts.fail("expected an order, got '" + ot + "'");
+        }
+    }
+    if (order < 1) ts.fail("order must be >= 1");
+    solid<Real> s(kind, order);
+    auto data = s.data();
+    for (std::size_t i = 0; i < data.size(); ++i) {
+        if (!ts.next(tok))
+            ts.fail("unexpected end of input; expected " + std::to_string(data.size()) + " values, got " +
+                    std::to_string(i));
+        std::size_t used = 0;
+        double v = 0;
+        try {
+            v = std::stod(tok, &used);
+            if (used != tok.size()) throw std::invalid_argument(tok);
+        } catch (const std::exception&) {
+            ts.fail("expected a number, got '" + tok + "'");
+        }
+        data[i] = static_cast<Real>(v);
+    }
+    return s;
+}
+
+/// Concatenated solids until end of input. As in the reference every solid is parsed by its
+/// own reader (io.cpp:124-129): line numbers in messages count from the solid's header line,
+/// and a solid starts on a fresh line.
+template <typename Real>
+std::vector<solid<Real>> read_solids(std::istream& is) {
+    std::vector<solid<Real>> out;
+    while (auto s = read_solid<Real>(is)) out.push_back(std::move(*s));
+    return out;
+}
+
+template <typename Real>
+std::vector<point_charge<Real>> read_charges(std::istream& is) {
+    std::vector<point_charge<Real>> out;
+    std::string line;
+    for (int line_no = 1; std::getline(is, line); ++line_no) {
+        const auto first = line.find_first_not_of(" \t\r");
+        if (first == std::string::npos || line[first] == '#') continue;
+        std::istringstream ls(line);
+        point_charge<Real> c{};
+        std::string rest;
+        if (!(ls >> c.position.x >> c.position.y >> c.position.z >> c.charge))
+            throw std::runtime_error("line " + std::to_string(line_no) + ": expected 'x y z q'");
+        if (ls >> rest)
+            throw std::runtime_error("line " + std::to_string(line_no) + ": trailing content '" + rest + "'");
+        out.push_back(c);
+    }
+    return out;
+}
+
+template <typename Real>
+void write_charges(std::ostream& os, std::span<const point_charge<Real>> charges) {
+    os.precision(std::numeric_limits<Real>::max_digits10);
+    for (const auto& c : charges)
+        os << c.position.x << ' ' << c.position.y << ' ' << c.position.z << ' ' << c.charge << '\n';
 }
 
 }  // namespace mpole_b200

@@ -218,6 +218,24 @@ sfmm_status sfmm_m2l_level_host(sfmm_handle* h, int64_t n_targets, const int64_t
                                 int64_t n_sources, int p_in, int p_out, const void* src_aos,
                                 void* out_aos);
 
+/* Pair list of one level of a uniform octree, in the form sfmm_plan_create and
+ * sfmm_m2l_level_host take (no reference counterpart: its callers issue one
+ * translation_request per pair, pipeline.hpp:15-21; tree traversal is a non-goal there).
+ * Targets: the boxes (i, j, k) of an nx x ny x nz grid of boxes of side box_size, target
+ * index (i ny + j) nz + k. Sources: the boxes of the grid extended by `halo` boxes on every
+ * side, index ((i + halo)(ny + 2 halo) + (j + halo))(nz + 2 halo) + (k + halo); halo = 3 holds
+ * every list entry (a level inside a larger domain), halo = 0 makes the targets their own
+ * sources and drops the entries outside the grid (a free-standing level). List of a target:
+ * the offsets d = source - target with d_a in [-2 - b_a, 3 - b_a], b_a the parity of the
+ * target's coordinate (the children of the parent's neighbours), without the near field
+ * max |d_a| <= 1: at most 189 entries, in lexicographic order of d; shift = -d box_size
+ * (source -> target centre). Call with tgt_ptr = src_index = shifts = NULL for the sizes
+ * (n_pairs, n_sources), then with arrays of n_targets + 1, n_pairs and 3 n_pairs entries
+ * (shifts in `precision`). Host arrays; no device work. */
+sfmm_status sfmm_level_pairs(int nx, int ny, int nz, int halo, double box_size,
+                             sfmm_precision precision, int64_t* tgt_ptr, int32_t* src_index,
+                             void* shifts, int64_t* n_pairs, int64_t* n_sources);
+
 /* Summation unit of sfmm_m2l_accumulate* for this order pair with the kernel the
  * handle would choose: 64 = pairs j and j+32 of a 64-pair group are added first,
  * then the 32 sums by the xor butterfly (lane distances 16, 8, 4, 2, 1); 32 or 16 =

@@ -16,6 +16,8 @@
 #include <cstring>
 #include <exception>
 #include <thread>
+#include <sstream>
+#include <cstdio>
 #include <vector>
 
 #include "mpole/mpole.hpp"
@@ -232,6 +234,40 @@ double ref_eval_local_f64(int order, const double* l, const double* center,
     std::memcpy(s.data().data(), l, solid_size(order) * sizeof(double));
     return eval_local<double>(s, {center[0], center[1], center[2]},
                               {x[0], x[1], x[2]});
+}
+
+// text format (io.hpp): write one solid / read concatenated solids through the reference
+long ref_write_solid_f64(int kind, int order, const double* data, char* buf, long cap) {
+    solid<double> s(static_cast<solid_kind>(kind), order);
+    std::memcpy(s.data().data(), data, solid_size(order) * sizeof(double));
+    std::ostringstream os;
+    write_solid<double>(os, s);
+    const std::string t = os.str();
+    if ((long)t.size() < cap) std::memcpy(buf, t.c_str(), t.size() + 1);
+    return (long)t.size();
+}
+// returns the number of solids (kinds / orders / concatenated data filled), or -1 with the
+// exception text in err
+int ref_read_solids_f64(const char* text, int max_solids, int* kinds, int* orders, double* data,
+                        long cap, char* err, int errcap) {
+    try {
+        std::istringstream is(text);
+        const auto v = read_solids<double>(is);
+        long pos = 0;
+        int n = 0;
+        for (const auto& s : v) {
+            if (n >= max_solids || pos + (long)s.data().size() > cap) break;
+            kinds[n] = static_cast<int>(s.kind());
+            orders[n] = s.order();
+            std::memcpy(data + pos, s.data().data(), s.data().size() * sizeof(double));
+            pos += (long)s.data().size();
+            ++n;
+        }
+        return n;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errcap, "%s", e.what());
+        return -1;
+    }
 }
 
 // single-precision forms of the three harmonics entry points

@@ -18,7 +18,7 @@ INCLUDE = PKG_DIR.parent / "include"
 LIB_PATH = PKG_DIR / "libsolidfmm_b200.so"
 
 SOURCES = ["sfmm_capi.cu", "sfmm_kernels.cu", "sfmm_tiled_f64.cu", "sfmm_tiled_f32.cu", "sfmm_mma_f64.cu", "sfmm_small.cu", "sfmm_harmonics.cu",
-           "tables.cpp"]
+           "tables.cpp", "level.cpp"]
 
 # -fmad=false: the kernels spell every fused multiply-add explicitly; nvcc must
 # not contract anything else (csrc/device_math.cuh).

@@ -59,6 +59,8 @@ _SIGNATURES = {
                                     c_int, c_void_p, c_void_p]),
     "sfmm_accumulation_unit": (c_int, [c_void_p, c_int, c_int]),
     "sfmm_harmonics_max_order": (c_int, []),
+    "sfmm_level_pairs": (c_int, [c_int, c_int, c_int, c_int, c_double, c_int, c_void_p, c_void_p,
+                                 c_void_p, POINTER(c_int64), POINTER(c_int64)]),
     "sfmm_p2m": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p,
                          c_int64, c_void_p]),
     "sfmm_eval_local": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_int,
@@ -172,6 +174,22 @@ def _ptr(a) -> c_void_p:
     if isinstance(a, np.ndarray):
         return a.ctypes.data_as(c_void_p)
     return c_void_p(int(a))
+
+
+def level_pairs(grid, halo: int = 3, box_size: float = 1.0, precision: int = F64):
+    """Pair list of one level of a uniform octree (sfmm_level_pairs): tgt_ptr, src_index,
+    shifts, n_sources."""
+    lib = load_library()
+    nx, ny, nz = (int(g) for g in grid)
+    n_pairs, n_sources = c_int64(0), c_int64(0)
+    check(lib.sfmm_level_pairs(nx, ny, nz, halo, box_size, precision, None, None, None,
+                               ctypes.byref(n_pairs), ctypes.byref(n_sources)))
+    tgt_ptr = np.empty(nx * ny * nz + 1, np.int64)
+    src_index = np.empty(n_pairs.value, np.int32)
+    shifts = np.empty((n_pairs.value, 3), dtype_of(precision))
+    check(lib.sfmm_level_pairs(nx, ny, nz, halo, box_size, precision, _ptr(tgt_ptr), _ptr(src_index),
+                               _ptr(shifts), ctypes.byref(n_pairs), ctypes.byref(n_sources)))
+    return tgt_ptr, src_index, shifts, n_sources.value
 
 
 class Handle:

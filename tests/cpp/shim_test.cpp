@@ -15,6 +15,8 @@ extern "C" {
 int orc_m2l_naive_f64(long n, int p_in, int p_out, const double* in, const double* shifts, double* out);
 int orc_translate_f64(int kind, long n, int p_in, int p_out, const double* in, const double* shifts, double* out);
 void orc_p2m_f64(int count, const double* charges, const double* center, int order, double* out);
+void orc_p2m_fma_f64(int count, const double* charges, const double* center, int order, double* out);
+double orc_eval_local_fma_f64(int order, const double* l, const double* center, const double* x);
 }
 
 using namespace mpole_b200;
@@ -268,6 +270,43 @@ int main() {
             });
         for (auto& th : threads) th.join();
         for (int t = 0; t < 4; ++t) CHECK(bad[t] == 0);
+    }
+    // p2m / eval_local on the device behind the reference's signatures (harmonics.hpp:36-51;
+    // field preservation as in test_pipeline.cpp:208-233)
+    {
+        const operator_data<double> ops(12);
+        workspace<double> ws(12);
+        std::uniform_real_distribution<double> ud(-0.5, 0.5);
+        std::vector<point_charge<double>> q(23);
+        for (auto& c : q) c = {{ud(rng), ud(rng), ud(rng)}, ud(rng) < 0 ? -1.0 : 1.0};
+        const vec3<double> centre{0.1, -0.2, 0.05};
+        const auto m = p2m<double>(ops, q, centre, 12);
+        solid<double> want(solid_kind::multipole, 12);
+        const double c3[3] = {centre.x, centre.y, centre.z};
+        orc_p2m_fma_f64((int)q.size(), &q[0].position.x, c3, 12, want.data().data());
+        CHECK(m.kind() == solid_kind::multipole && m == want);
+        const vec3<double> shift{3.0, -2.5, 4.0};
+        const auto l = m2l(ops, m, shift, 12, ws);
+        const vec3<double> lc = centre + shift, x{lc.x + 0.2, lc.y - 0.1, lc.z + 0.15};
+        const double phi = eval_local<double>(ops, l, lc, x);
+        const double lc3[3] = {lc.x, lc.y, lc.z}, x3[3] = {x.x, x.y, x.z};
+        CHECK(phi == orc_eval_local_fma_f64(12, l.data().data(), lc3, x3));
+        double direct = 0;
+        for (const auto& c : q) direct += c.charge / norm(x - c.position);
+        CHECK(std::abs(phi - direct) < 1e-7 * std::abs(direct) + 1e-9);
+        // batched forms
+        const std::int64_t ptr[4] = {0, 5, 5, 23};
+        const vec3<double> cs[3] = {centre, {1, 1, 1}, {-1, 0, 2}};
+        const auto ms = p2m<double>(ops, q, ptr, cs, 7);
+        CHECK(ms.size() == 3);
+        for (auto v : ms[1].data()) CHECK(v == 0.0);
+        bool threw = false;
+        try {
+            p2m<double>(ops, q, centre, 13);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASSED", failures);
     return failures ? 1 : 0;

@@ -32,3 +32,21 @@ def test_reference_pipeline_cases_through_the_shim(tmp_path):
     res = subprocess.run([str(exe)], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, timeout=600)
     assert res.returncode == 0, res.stdout
     assert "ALL PASSED" in res.stdout
+
+
+def test_text_io_matches_the_reference_tool(tmp_path):
+    """SOLID / charge text format of the shim against the reference's io.cpp (CPU only; needs
+    the compiled reference, which is built here and travels with the snapshot)."""
+    ref = ROOT / "oracle" / "_ref" / "libmpole_ref.so"
+    if not ref.exists():
+        oracle_lib.Reference.try_load("fma")
+    if not ref.exists():
+        pytest.skip("oracle/_ref is not built")
+    lib_dir = build.LIB_PATH.parent
+    exe = tmp_path / "io_test"
+    cmd = ["g++", "-std=c++20", "-O1", f"-I{ROOT / 'include'}", "-o", str(exe),
+           str(ROOT / "tests" / "cpp" / "io_test.cpp"), f"-L{lib_dir}", "-lsolidfmm_b200",
+           f"-L{ref.parent}", "-lmpole_ref", f"-Wl,-rpath,{lib_dir}", f"-Wl,-rpath,{ref.parent}", "-pthread"]
+    subprocess.run(cmd, check=True, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    res = subprocess.run([str(exe)], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, timeout=120)
+    assert res.returncode == 0 and "ALL PASSED" in res.stdout, res.stdout

@@ -191,3 +191,36 @@ def test_compact_sources_is_a_relabelling():
     assert np.array_equal(used[remapped], idx)
     src = rng.standard_normal((500, 6))
     assert np.array_equal(src[used][remapped], src[idx])
+
+
+def test_level_pairs_is_the_189_offset_interaction_list():
+    """sfmm_level_pairs (N3): the embedded level (halo 3) equals the generator of the bench
+    workload (workloads.config3 index arithmetic) entry for entry; the free-standing level
+    (halo 0) equals a brute-force enumeration; sizes-only call; argument checks."""
+    from paper_2202_02847_b200 import capi, workloads
+    gx, gy, gz = 5, 4, 6
+    tgt_ptr, src_index, shifts, ns = capi.level_pairs((gx, gy, gz), halo=3, box_size=0.5)
+    assert ns == (gx + 6) * (gy + 6) * (gz + 6) and len(tgt_ptr) == gx * gy * gz + 1
+    assert np.array_equal(tgt_ptr, np.arange(gx * gy * gz + 1) * 189)
+    sy, sz = gy + 6, gz + 6
+    for t in (0, 7, 53, gx * gy * gz - 1):
+        tx, ty, tz = t // (gy * gz), (t // gz) % gy, t % gz
+        off = workloads.interaction_offsets((tx & 1, ty & 1, tz & 1))
+        want = ((tx + off[:, 0] + 3) * sy + (ty + off[:, 1] + 3)) * sz + (tz + off[:, 2] + 3)
+        assert np.array_equal(src_index[t * 189:(t + 1) * 189], want)
+        assert np.array_equal(shifts[t * 189:(t + 1) * 189], -0.5 * off)
+    # free-standing level: entries outside the grid are dropped, sources = targets
+    tp, si, sh, ns0 = capi.level_pairs((gx, gy, gz), halo=0, box_size=1.0, precision=capi.F32)
+    assert ns0 == gx * gy * gz and sh.dtype == np.float32
+    for t in range(gx * gy * gz):
+        tx, ty, tz = t // (gy * gz), (t // gz) % gy, t % gz
+        off = workloads.interaction_offsets((tx & 1, ty & 1, tz & 1))
+        s = np.array([tx, ty, tz]) + off
+        ok = np.all((s >= 0) & (s < [gx, gy, gz]), axis=1)
+        assert np.array_equal(si[tp[t]:tp[t + 1]], ((s[ok, 0] * gy + s[ok, 1]) * gz + s[ok, 2]))
+        assert np.array_equal(sh[tp[t]:tp[t + 1]], -off[ok].astype(np.float32))
+    assert tp[-1] == len(si) > 0
+    with pytest.raises(capi.InvalidArgument):
+        capi.level_pairs((0, 1, 1))
+    with pytest.raises(capi.InvalidArgument):
+        capi.level_pairs((2, 2, 2), box_size=0.0)
