@@ -3,10 +3,11 @@
 //   L2P        potential of a local expansion at a point    (reference harmonics.cpp:119-152)
 // both built on the regular solid harmonics R_n^m (harmonics.cpp:18-50).
 //
-// Mapping: one warp per box (P2M) or per evaluation point (L2P), lane = m. The reference's
-// recurrences run in n for a fixed m ((n^2 - m^2) R_n^m = (2n-1) z R_{n-1}^m - |r|^2 R_{n-2}^m)
-// once the diagonal R_m^m is known, so a lane carries R_{n-1}^m and R_{n-2}^m in two registers
-// each and no triangle is ever stored. The operation order and the fused multiply-adds are
+// Mapping: a lane owns columns m of the triangle. The reference's recurrences run in n for a
+// fixed m ((n^2 - m^2) R_n^m = (2n-1) z R_{n-1}^m - |r|^2 R_{n-2}^m) once the diagonal R_m^m is
+// known, so a lane carries R_{n-1}^m and R_{n-2}^m in two registers each and no triangle of
+// harmonics is ever stored; lane l takes the columns l and P-1-l (P+1 coefficients whatever l
+// is), ceil(P/2) lanes serve one box (P2M) or one point (L2P). The operation order and the fused multiply-adds are
 // those of the reference built with -mfma -ffp-contract=fast (the parity build, DESIGN.md §2;
 // read off its object code and pinned by tests/test_oracle.py):
 //   |r|^2          = fma(z, z, fma(x, x, y*y))
@@ -16,6 +17,7 @@
 //   L2P            : total = fma(L_n^0, R_n^0, total) ; row = row + fma(Lre, Rre, Lim*Rim), m
 //                    ascending from 0 ; total = total + (row + row), n ascending
 // Compiled with -fmad=false: every fused operation below is explicit.
+#include <algorithm>
 #include <cfloat>
 
 #include "device_math.cuh"
@@ -49,53 +51,6 @@ __device__ __forceinline__ bool effectively_zero(Real x, Real y, Real z) {
     return n < real_min<Real>();
 }
 
-// R_n^m of one point for m = lane, produced row by row.
-template <typename Real>
-struct RegularColumn {
-    Real x, y, z, r2;
-    Real p1re, p1im, p2re, p2im;  // R_{n-1}^m, R_{n-2}^m
-    bool zero;                    // |r| effectively zero: R_0^0 = 1 and nothing else
-
-    // inv2n[n] = 1 / (2n), shared by the block
-    __device__ void start(Real x_, Real y_, Real z_, int m, const Real* inv2n) {
-        x = x_, y = y_, z = z_;
-        zero = effectively_zero(x, y, z);
-        r2 = fma_(z, z, fma_(x, x, y * y));
-        // diagonal up to R_m^m
-        Real re = Real(1), im = Real(0);
-        for (int n = 1; n <= m; ++n) {
-            const Real nre = inv2n[n] * fma_(-y, im, x * re);
-            const Real nim = inv2n[n] * fma_(x, im, y * re);
-            re = nre;
-            im = nim;
-        }
-        p1re = re, p1im = im;  // consumed by row(m, ...)
-        p2re = p2im = Real(0);
-    }
-    // row n >= m, called with n ascending; denom = 1 / (n^2 - m^2) (unused for n == m)
-    __device__ void row(int n, int m, Real denom, Real& re, Real& im) {
-        if (n == m) {
-            re = p1re;
-            im = p1im;
-        } else {
-            const Real zf = Real(2 * n - 1) * z;
-            Real a = zf * p1re, b = zf * p1im;
-            if (n - 2 >= m) {
-                a = fma_(-r2, p2re, a);
-                b = fma_(-r2, p2im, b);
-            }
-            re = denom * a;
-            im = m == 0 ? Real(0) : denom * b;
-            p2re = p1re, p2im = p1im;
-            p1re = re, p1im = im;
-        }
-        if (zero) {
-            re = (n == 0) ? Real(1) : Real(0);
-            im = Real(0);
-        }
-    }
-};
-
 // position of (n, m, part) in the output layouts
 __device__ __forceinline__ int64_t out_index(int layout, int64_t b, int n, int m, int part, int order,
                                              int64_t stride) {
@@ -105,92 +60,245 @@ __device__ __forceinline__ int64_t out_index(int layout, int64_t b, int n, int m
     return b * ((int64_t)order * (order + 1)) + c;
 }
 
-template <typename Real, int NMAX>
-__global__ void __launch_bounds__(128)
+// P2M. A box is worked on by ceil(P/2) lanes: lane l owns the columns m = l and m = P-1-l of
+// the triangle, P+1 coefficients together whatever l is (the triangle is balanced by pairing
+// its longest column with its shortest), so a warp holds floor(32 / ceil(P/2)) boxes and almost
+// every lane is busy (P = 20: 3 boxes, 30 lanes, 21 coefficients each). The coefficients of a
+// lane are numbered by "slots" s = 0..P: first the rows n = m .. P-1 of its long column, then
+// those of the short one; the slot loop is unrolled, so the accumulators, the reciprocals
+// 1/(n^2-m^2) and the two-term recurrence state stay in registers. Charges are taken in list
+// order (the accumulation M = fma(q, R, M) is a chain in the reference too); two charges are in
+// flight per trip for instruction-level parallelism.
+// state of one charge in the slot loop of p2m_kernel
+template <typename Real>
+struct ChargeState {
+    Real q, z, r2, dre, dim, p1re, p1im, p2re, p2im;
+    bool zero;
+    // loads the charge, runs the diagonal recurrence up to R_mtop^mtop and leaves R_mA^mA in p1
+    __device__ __forceinline__ void start(Real x, Real y, Real z_, Real q_, int mA, int mtop, const Real* inv2n) {
+        q = q_, z = z_;
+        zero = effectively_zero(x, y, z);
+        r2 = fma_(z, z, fma_(x, x, y * y));
+        dre = Real(1), dim = Real(0);
+        p1re = Real(1), p1im = Real(0);
+        for (int n = 1; n <= mtop; ++n) {
+            const Real nre = inv2n[n] * fma_(-y, dim, x * dre);
+            const Real nim = inv2n[n] * fma_(x, dim, y * dre);
+            dre = nre;
+            dim = nim;
+            if (n == mA) p1re = dre, p1im = dim;
+        }
+        p2re = p2im = Real(0);
+    }
+    // coefficient (n, m) = row k of the current column; `first` = first slot of the short column
+    __device__ __forceinline__ void slot(int n, int m, int k, bool first, Real den, Real& re, Real& im) {
+        if (first) p1re = dre, p1im = dim;
+        const Real zf = Real(2 * n - 1) * z;
+        Real a = zf * p1re, c = zf * p1im;
+        const Real a2 = fma_(-r2, p2re, a), c2 = fma_(-r2, p2im, c);
+        a = k >= 2 ? a2 : a;
+        c = k >= 2 ? c2 : c;
+        re = den * a;
+        im = m == 0 ? Real(0) : den * c;
+        re = k == 0 ? p1re : re;
+        im = k == 0 ? p1im : im;
+        p2re = k == 0 ? p2re : p1re;
+        p2im = k == 0 ? p2im : p1im;
+        p1re = re, p1im = im;
+        if (zero) {
+            re = n == 0 ? Real(1) : Real(0);
+            im = Real(0);
+        }
+    }
+};
+
+// P2M. A box is worked on by ceil(P/2) lanes: lane l owns the columns m = l and m = P-1-l of
+// the triangle, P+1 coefficients together whatever l is (the triangle is balanced by pairing
+// its longest column with its shortest), so a warp holds floor(32 / ceil(P/2)) boxes and almost
+// every lane is busy (P = 20: 3 boxes, 30 lanes, 21 coefficients each). The coefficients of a
+// lane are numbered by "slots" s = 0..P: first the rows n = m .. P-1 of its long column, then
+// those of the short one; the slot loop is unrolled, so the accumulators and the two-term
+// recurrence state stay in registers (the reciprocals 1/(n^2-m^2) come from a shared table).
+// Charges are taken in list order (M = fma(q, R, M) is a chain in the reference too); the
+// recurrences of two consecutive charges run side by side (they are latency bound), and the
+// next pair is loaded while the current one computes.
+template <typename Real, int PM>
+__global__ void __launch_bounds__(128, PM <= 20 ? 3 : 2)
 p2m_kernel(const int64_t* __restrict__ box_ptr, const Real* __restrict__ charges,
            const Real* __restrict__ centers, int64_t n_boxes, int order, int layout,
            Real* __restrict__ out, int64_t stride) {
     __shared__ Real inv2n[kHarmMaxOrder + 1];
+    __shared__ Real denom_tab[(PM + 1) * (PM + 1)];  // [n][m]
+    constexpr int LD = PM + 1;
     if (threadIdx.x <= kHarmMaxOrder) inv2n[threadIdx.x] = threadIdx.x ? Real(1) / Real(2 * (int)threadIdx.x) : Real(0);
-    __syncthreads();
-    const int m = threadIdx.x & 31;
-    const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (b >= n_boxes || m >= order) return;
-    Real denom[NMAX], are[NMAX], aim[NMAX];
-#pragma unroll
-    for (int k = 0; k < NMAX; ++k) {
-        const int n = m + k;
-        denom[k] = k ? Real(1) / Real(n * n - m * m) : Real(0);
-        are[k] = aim[k] = Real(0);
+    for (int i = threadIdx.x; i < LD * LD; i += blockDim.x) {
+        const int n = i / LD, mm = i - n * LD;
+        denom_tab[i] = mm < n ? Real(1) / Real(n * n - mm * mm) : Real(0);
     }
-    const Real cx = centers[3 * b], cy = centers[3 * b + 1], cz = centers[3 * b + 2];
-    for (int64_t j = box_ptr[b]; j < box_ptr[b + 1]; ++j) {
-        const Real q = charges[4 * j + 3];
-        RegularColumn<Real> col;
-        col.start(charges[4 * j] - cx, charges[4 * j + 1] - cy, charges[4 * j + 2] - cz, m, inv2n);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int half = (order + 1) >> 1, per_warp = 32 / half;
+    const int sub = lane / half, l = lane - sub * half;
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t b = warp * per_warp + sub;
+    if (sub >= per_warp || b >= n_boxes) return;
+    const int mA = l, mB = order - 1 - l;
+    const int cA = order - mA;                   // slots of the long column
+    const int total = mB > mA ? order + 1 : cA;  // odd orders: the middle column stands alone
+    const int mtop = mB > mA ? mB : mA;
+    Real are[PM + 1], aim[PM + 1];
 #pragma unroll
-        for (int k = 0; k < NMAX; ++k) {
-            if (m + k < order) {
-                Real re, im;
-                col.row(m + k, m, denom[k], re, im);
-                are[k] = fma_(q, re, are[k]);
-                aim[k] = fma_(q, im, aim[k]);
+    for (int s = 0; s <= PM; ++s) are[s] = aim[s] = Real(0);
+    const Real cx = centers[3 * b], cy = centers[3 * b + 1], cz = centers[3 * b + 2];
+    const int64_t j0 = box_ptr[b], j1 = box_ptr[b + 1];
+    // charge pair (j, j + 1); the data of the next pair is in flight during the slot loop
+    Real nx[2], ny[2], nz[2], nq[2];
+    auto fetch = [&](int64_t j) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t jj = j + u < j1 ? j + u : (j1 > j0 ? j1 - 1 : j0);
+            const bool ok = j + u < j1;
+            nx[u] = ok ? charges[4 * jj] : Real(0);
+            ny[u] = ok ? charges[4 * jj + 1] : Real(0);
+            nz[u] = ok ? charges[4 * jj + 2] : Real(0);
+            nq[u] = ok ? charges[4 * jj + 3] : Real(0);
+        }
+    };
+    if (j0 < j1) fetch(j0);
+    for (int64_t j = j0; j < j1; j += 2) {
+        ChargeState<Real> c0, c1;
+        const bool two = j + 1 < j1;
+        c0.start(nx[0] - cx, ny[0] - cy, nz[0] - cz, nq[0], mA, mtop, inv2n);
+        c1.start(nx[1] - cx, ny[1] - cy, nz[1] - cz, nq[1], mA, mtop, inv2n);
+        if (j + 2 < j1) fetch(j + 2);
+#pragma unroll
+        for (int s = 0; s <= PM; ++s) {
+            if (s < total) {
+                const bool second = s >= cA;
+                const int m = second ? mB : mA, k = second ? s - cA : s, n = m + k;
+                const Real den = denom_tab[n * LD + m];
+                Real re0, im0, re1, im1;
+                c0.slot(n, m, k, s == cA, den, re0, im0);
+                c1.slot(n, m, k, s == cA, den, re1, im1);
+                are[s] = fma_(c0.q, re0, are[s]);
+                aim[s] = fma_(c0.q, im0, aim[s]);
+                if (two) {
+                    are[s] = fma_(c1.q, re1, are[s]);
+                    aim[s] = fma_(c1.q, im1, aim[s]);
+                }
             }
         }
     }
 #pragma unroll
-    for (int k = 0; k < NMAX; ++k) {
-        const int n = m + k;
-        if (n < order) {
-            out[out_index(layout, b, n, m, 0, order, stride)] = are[k];
-            out[out_index(layout, b, n, m, 1, order, stride)] = aim[k];
+    for (int s = 0; s <= PM; ++s) {
+        if (s < total) {
+            const int m = s < cA ? mA : mB, n = m + (s < cA ? s : s - cA);
+            out[out_index(layout, b, n, m, 0, order, stride)] = are[s];
+            out[out_index(layout, b, n, m, 1, order, stride)] = aim[s];
         }
     }
     // padding of the rows layout (rows of odd length carry two zeros)
-    if (layout == LAYOUT_ROWS && m == 0) {
+    if (layout == LAYOUT_ROWS && l == 0) {
         for (int n = 0; n < order; ++n)
             for (int k = 2 * (n + 1); k < rows_off(n + 1) - rows_off(n); ++k)
                 out[b * rows_off(order) + rows_off(n) + k] = Real(0);
     }
 }
 
-// L2P: out[i] = paired_sum(L[box(i)], regular(x_i - centre[box(i)])) (harmonics.cpp:119-152)
+// L2P: out[i] = paired_sum(L[box(i)], regular(x_i - centre[box(i)])) (harmonics.cpp:119-152).
+// Same lane mapping as P2M: ceil(P/2) lanes per point, lane l owns the columns m = l and
+// m = P-1-l, a warp works on floor(32 / ceil(P/2)) consecutive points at a time and walks a
+// contiguous range of points. The local expansion of the current box of every sub-group stays
+// in shared memory (points of one box usually follow one another). The sum over m of a row is
+// taken in ascending m like the reference's loop: the terms L_n^m * conj R_n^m go through shared
+// memory, lane l then adds the rows l and P-1-l (again P-1 additions whatever l is), and the
+// first lane of the sub-group folds the rows in ascending n.
+// dynamic shared memory: denom [P][P+1] | per warp and sub-group: locals [P(P+1)], terms
+// [P(P+1)/2], rows [P]
+extern __shared__ __align__(16) unsigned char harm_smem[];
 template <typename Real>
 __global__ void __launch_bounds__(128)
 eval_local_kernel(const int32_t* __restrict__ point_box, const Real* __restrict__ points,
                   const Real* __restrict__ centers, int64_t n_points, int64_t n_boxes, int order,
                   int layout, const Real* __restrict__ locals, int64_t stride, Real* __restrict__ out) {
     __shared__ Real inv2n[kHarmMaxOrder + 1];
+    const int LD = order + 1, S = order * (order + 1);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int half = (order + 1) >> 1, per_warp = 32 / half;
+    const int sub = lane / half, l = lane - sub * half;
+    const bool lane_on = sub < per_warp;
+    const size_t per_sub = (size_t)S + (size_t)S / 2 + order;  // locals, terms (triangle), rows
+    Real* denom = reinterpret_cast<Real*>(harm_smem);
+    Real* my_loc = denom + order * LD + ((size_t)w * per_warp + (lane_on ? sub : 0)) * per_sub;
+    Real* my_terms = my_loc + S;
+    Real* my_rows = my_terms + S / 2;
     if (threadIdx.x <= kHarmMaxOrder) inv2n[threadIdx.x] = threadIdx.x ? Real(1) / Real(2 * (int)threadIdx.x) : Real(0);
-    __syncthreads();
-    const int m = threadIdx.x & 31;
-    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (i >= n_points) return;  // whole warps leave together
-    const int64_t b = point_box ? (int64_t)point_box[i] : i;
-    const bool lane_on = m < order;
-    RegularColumn<Real> col;
-    col.start(points[3 * i] - centers[3 * b], points[3 * i + 1] - centers[3 * b + 1],
-              points[3 * i + 2] - centers[3 * b + 2], lane_on ? m : 0, inv2n);
-    Real total = Real(0);
-    for (int n = 0; n < order; ++n) {
-        Real term = Real(0), lre0 = Real(0), vre0 = Real(0);
-        if (lane_on && m <= n) {
-            Real vre, vim;
-            const Real denom = n > m ? Real(1) / Real(n * n - m * m) : Real(0);
-            col.row(n, m, denom, vre, vim);
-            const Real lre = locals[out_index(layout, b, n, m, 0, order, stride)];
-            const Real lim = locals[out_index(layout, b, n, m, 1, order, stride)];
-            term = fma_(lre, vre, lim * vim);
-            lre0 = lre, vre0 = vre;
-        }
-        // ordered sum over m = 1..n on every lane (the lanes stay in lockstep)
-        Real rowsum = Real(0);
-        for (int k = 1; k <= n; ++k) rowsum = rowsum + __shfl_sync(0xffffffffu, term, k);
-        const Real l0 = __shfl_sync(0xffffffffu, lre0, 0), v0 = __shfl_sync(0xffffffffu, vre0, 0);
-        total = fma_(l0, v0, total);
-        total = total + (rowsum + rowsum);
+    for (int i = threadIdx.x; i < order * LD; i += blockDim.x) {
+        const int n = i / LD, mm = i - n * LD;
+        denom[i] = (mm < n) ? Real(1) / Real(n * n - mm * mm) : Real(0);
     }
-    if (m == 0) out[i] = total;
+    __syncthreads();
+    const int mA = l, mB = order - 1 - l;
+    const int cA = order - mA;
+    const int total = mB > mA ? order + 1 : cA;
+    const int mtop = mB > mA ? mB : mA;
+    const int64_t warps = (int64_t)gridDim.x * 4, wid = (int64_t)blockIdx.x * 4 + w;
+    int64_t chunk = (n_points + warps - 1) / warps;
+    chunk = (chunk + per_warp - 1) / per_warp * per_warp;
+    const int64_t i0 = wid * chunk, i1 = i0 + chunk < n_points ? i0 + chunk : n_points;
+    int64_t cached = -1;
+    for (int64_t base = i0; base < i1; base += per_warp) {
+        const int64_t i = base + sub;
+        const bool on = lane_on && i < i1;
+        const int64_t b = on ? (point_box ? (int64_t)point_box[i] : i) : -1;
+        if (on && b != cached) {  // the lanes of a sub-group agree
+            if (layout == LAYOUT_AOS) {
+                for (int c = l; c < S; c += half) my_loc[c] = locals[b * S + c];
+            } else {
+                for (int n = 0; n < order; ++n)
+                    for (int c = l; c < 2 * (n + 1); c += half)
+                        my_loc[n * (n + 1) + c] = locals[out_index(layout, b, n, c >> 1, c & 1, order, stride)];
+            }
+            cached = b;
+        }
+        __syncwarp();
+        if (on) {
+            ChargeState<Real> st;
+            st.start(points[3 * i] - centers[3 * b], points[3 * i + 1] - centers[3 * b + 1],
+                     points[3 * i + 2] - centers[3 * b + 2], Real(0), mA, mtop, inv2n);
+            for (int s = 0; s < total; ++s) {
+                const bool second = s >= cA;
+                const int m = second ? mB : mA, k = second ? s - cA : s, n = m + k;
+                Real vre, vim;
+                st.slot(n, m, k, s == cA, denom[n * LD + m], vre, vim);
+                const Real lre = my_loc[n * (n + 1) + 2 * m], lim = my_loc[n * (n + 1) + 2 * m + 1];
+                // column 0 keeps the two factors apart: total = fma(L_n^0, R_n^0, total)
+                my_terms[n * (n + 1) / 2 + m] = m == 0 ? vre : fma_(lre, vre, lim * vim);
+            }
+        }
+        __syncwarp();
+        if (on) {
+            // rows l and P-1-l, each in ascending m
+            for (int pass = 0; pass < 2; ++pass) {
+                const int n = pass ? mB : mA;
+                if (pass && mB <= mA) break;
+                Real rowsum = Real(0);
+                for (int k = 1; k <= n; ++k) rowsum = rowsum + my_terms[n * (n + 1) / 2 + k];
+                my_rows[n] = rowsum;
+            }
+        }
+        __syncwarp();
+        if (on && l == 0) {
+            Real total_sum = Real(0);
+            for (int n = 0; n < order; ++n) {
+                total_sum = fma_(my_loc[n * (n + 1)], my_terms[n * (n + 1) / 2], total_sum);
+                const Real r = my_rows[n];
+                total_sum = total_sum + (r + r);
+            }
+            out[i] = total_sum;
+        }
+        __syncwarp();
+    }
 }
 
 }  // namespace
@@ -201,15 +309,19 @@ cudaError_t launch_p2m(const int64_t* box_ptr, const Real* charges, const Real* 
                        cudaStream_t stream) {
     if (n_boxes <= 0) return cudaSuccess;
     if (order > kHarmMaxOrder) return cudaErrorInvalidValue;
-    const unsigned grid = (unsigned)((n_boxes + 3) / 4);
-    if (order <= 8)
-        p2m_kernel<Real, 8><<<grid, 128, 0, stream>>>(box_ptr, charges, centers, n_boxes, order, layout, out, stride);
-    else if (order <= 16)
-        p2m_kernel<Real, 16><<<grid, 128, 0, stream>>>(box_ptr, charges, centers, n_boxes, order, layout, out, stride);
-    else if (order <= 24)
-        p2m_kernel<Real, 24><<<grid, 128, 0, stream>>>(box_ptr, charges, centers, n_boxes, order, layout, out, stride);
-    else
-        p2m_kernel<Real, 32><<<grid, 128, 0, stream>>>(box_ptr, charges, centers, n_boxes, order, layout, out, stride);
+    const int per_warp = 32 / ((order + 1) / 2);
+    const int64_t warps = (n_boxes + per_warp - 1) / per_warp;
+    const unsigned grid = (unsigned)((warps + 3) / 4);
+#define SFMM_P2M(PM)                                                                                  \
+    p2m_kernel<Real, PM><<<grid, 128, 0, stream>>>(box_ptr, charges, centers, n_boxes, order, layout, \
+                                                   out, stride)
+    if (order <= 8) SFMM_P2M(8);
+    else if (order <= 12) SFMM_P2M(12);
+    else if (order <= 16) SFMM_P2M(16);
+    else if (order <= 20) SFMM_P2M(20);
+    else if (order <= 24) SFMM_P2M(24);
+    else SFMM_P2M(32);
+#undef SFMM_P2M
     return cudaGetLastError();
 }
 
@@ -219,8 +331,19 @@ cudaError_t launch_eval_local(const int32_t* point_box, const Real* points, cons
                               const Real* locals, int64_t stride, Real* out, cudaStream_t stream) {
     if (n_points <= 0) return cudaSuccess;
     if (order > kHarmMaxOrder) return cudaErrorInvalidValue;
-    const unsigned grid = (unsigned)((n_points + 3) / 4);
-    eval_local_kernel<Real><<<grid, 128, 0, stream>>>(point_box, points, centers, n_points, n_boxes, order,
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_warp = 32 / ((order + 1) / 2);
+    const size_t smem = sizeof(Real) * ((size_t)order * (order + 1) +
+                                        4 * per_warp * ((size_t)order * (order + 1) * 3 / 2 + order));
+    cudaError_t e = cudaFuncSetAttribute(eval_local_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_local_kernel<Real>, 128, smem);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (unsigned)std::min<int64_t>((n_points + 3) / 4, (int64_t)sms * std::max(per_sm, 1));
+    eval_local_kernel<Real><<<grid, 128, smem, stream>>>(point_box, points, centers, n_points, n_boxes, order,
                                                       layout, locals, stride, out);
     return cudaGetLastError();
 }
