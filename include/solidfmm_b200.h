@@ -249,7 +249,12 @@ int sfmm_accumulation_unit(const sfmm_handle* h, int p_in, int p_out);
  * (default), 1 = generic kernel (any order), 2 = tiled kernel (orders <= 20
  * double / <= 18 single; INVALID_ARGUMENT at call time beyond that), 3 = FP64
  * tensor-core kernel (double precision, handle order <= 30), 4 = small-order kernel
- * (same order <= 8, independent translations). */
+ * (same order <= 8, independent translations). "accumulate_plain": how the tiled kernel adds
+ * the 64-pair groups of a target (all groups of a target run in one CTA, in ascending order,
+ * so every sum has one owner at a time and the order is fixed): 0 (default) = the owner sends
+ * the sums of the later groups to the L2 to be added there (red.global.add.f64, no round
+ * trip); 1 = the owner loads, adds and stores (no atomic or reduction instruction anywhere;
+ * 4 % slower on the P = 20 level). Same bits either way. Single precision always uses 1. */
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value);
 
 /* Measures the FMA-pipe peak (TFLOP/s, 2 flops per FMA) of the handle's device

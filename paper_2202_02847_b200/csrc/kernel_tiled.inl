@@ -588,6 +588,8 @@ __device__ __forceinline__ void lane_transpose_sum(Real (&v)[NV], int lane) {
 }
 
 constexpr int CHK = 4;  // elements per butterfly of phase D
+// output mode of the tiled kernel: plain stores | accumulate, load-add-store | accumulate, L2 add
+enum : int { ACC_NONE = 0, ACC_PLAIN = 1, ACC_L2ADD = 2 };
 
 __device__ __forceinline__ int ld_volatile_shared(const int* p) {
     return *reinterpret_cast<const volatile int*>(p);
@@ -644,11 +646,11 @@ __device__ __forceinline__ void load4_cg(const float* p, float (&x)[4]) {
 __device__ __forceinline__ void add_ordered(double* dst, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(dst), "d"(v) : "memory");
 }
-__device__ __forceinline__ void add_ordered(float* dst, float v) { __stcg(dst, __ldcg(dst) + v); }
+__device__ __forceinline__ void add_ordered(float* dst, float v) { __stcg(dst, __ldcg(dst) + v); }  // unused: f32 runs ACC_PLAIN
 
 // ROWS: the sources are in LAYOUT_ROWS (sfmm_internal.hpp): a lane reads re, im of two
 // consecutive m of its own source with one load and touches whole sectors only.
-template <int TL, bool ACC, bool ROWS>
+template <int TL, int ACC, bool ROWS>
 __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int gen, int flags) {
     constexpr int L = 32 * TL;
     constexpr int CHA = 2;  // elements per batch of phase-A loads
@@ -760,10 +762,32 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
                 c[t] = Real(1);
                 s[t] = Real(0);
             }
+            // accumulate mode: after the butterfly of a chunk, lanes REP k .. REP k + REP-1 hold
+            // value k of the chunk (element k >> 1, part k & 1); the first of them owns the
+            // running sum of that coefficient. The groups of a target follow one another in this
+            // CTA (barriers in between), so a sum has one owner at a time and the order of the
+            // additions is fixed; the first group stores 0 + sum as reduce_groups_kernel starts
+            // (same signed zeros). Later groups either
+            //   ACC_L2ADD  send their sum to the L2 to be added there (red.global.add.f64 by the
+            //              single owner: no round trip, 5.81 ms per level), or
+            //   ACC_PLAIN  load, add and store (no atomic or reduction instruction at all; the
+            //              load of the next chunk is in flight during the current one, 6.07 ms).
+            // Both give the same bits (one rounding per addition, same order).
+            constexpr int NV = 2 * CHK, REP = 32 / NV;
+            // ACC_PLAIN: this lane's element of the current chunk, its running sum and where it lives
+            const int acc_k = lane / REP;
+            const bool acc_lane = ACC == ACC_PLAIN && !(lane & (REP - 1));
+            int acc_m = acc_k >> 1;
+            Real* acc_dst = nullptr;
+            Real prev_cur = Real(0);
+            if constexpr (ACC == ACC_PLAIN) {
+                acc_dst = out_d + (int64_t)(aos_re(n, 0) + 2 * (acc_k >> 1) + (acc_k & 1)) * e.out_stride;
+                // (column 0 has no imaginary part: never read, never written)
+                if (acc_lane && !first_d && acc_m <= n && !((acc_k & 1) && acc_m == 0)) prev_cur = __ldcg(acc_dst);
+            }
             while (ld_volatile_shared(&row_done[n]) != 2 * gen) __nanosleep(32);
             __threadfence_block();
             for (int m0 = 0; m0 <= n; m0 += CHK) {
-                constexpr int NV = 2 * CHK, REP = 32 / NV;
                 Real v[NV];
 #pragma unroll
                 for (int j = 0; j < NV; ++j) v[j] = Real(0);
@@ -798,16 +822,23 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
                     v[2 * u] = sr;
                     v[2 * u + 1] = si;
                 }
-                if constexpr (ACC) {
+                if constexpr (ACC == ACC_PLAIN) {
+                    // what the previous groups left for the NEXT chunk is requested before this
+                    // chunk's butterfly: its L2 latency hides behind a whole trip of the loop
+                    Real prev_nxt = Real(0);
+                    const bool w_nxt = acc_lane && !first_d && acc_m + CHK <= n;
+                    if (w_nxt) prev_nxt = __ldcg(acc_dst + (int64_t)(2 * CHK) * e.out_stride);
+                    lane_transpose_sum<NV>(v, lane);
+                    if (acc_lane && acc_m <= n && !((acc_k & 1) && acc_m == 0)) __stcg(acc_dst, prev_cur + v[0]);
+                    prev_cur = prev_nxt;
+                    acc_m += CHK;
+                    acc_dst += (int64_t)(2 * CHK) * e.out_stride;
+                } else if constexpr (ACC == ACC_L2ADD) {
                     lane_transpose_sum<NV>(v, lane);
                     // lanes REP k .. REP k + REP-1 hold value k: element k >> 1, part k & 1
                     const int k = lane / REP, m = m0 + (k >> 1), part = k & 1;
                     if (!(lane & (REP - 1)) && m <= n && !(part && m == 0)) {
                         Real* dst = out_d + (int64_t)(aos_re(n, m) + part) * e.out_stride;
-                        // 0 + first group, as reduce_groups_kernel starts (same signed zeros);
-                        // later groups add at the L2 (no round trip; the store and the
-                        // reductions of one address are ordered by the barriers between the
-                        // groups). red.f32 would flush subnormals: read-modify-write there
                         if (first_d) __stcg(dst, Real(0) + v[0]);
                         else add_ordered(dst, v[0]);
                     }
@@ -850,7 +881,7 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
     }
 }
 
-template <int TL, bool ACC, bool ROWS>
+template <int TL, int ACC, bool ROWS>
 __global__ void __launch_bounds__(SFMM_MAXTHREADS, 1)
 translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, int p_rot,
                        int tab_len) {
@@ -1142,8 +1173,13 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     if (n_groups >= INT_MAX || a.n_targets >= INT_MAX) return cudaErrorInvalidValue;
     const int block = 32 * tiled_warps_for(p_rot);
     const bool acc = a.src_index != nullptr, rows = a.in_layout == LAYOUT_ROWS;
-    auto kern = acc ? (rows ? translate_tiled_kernel<TL, true, true> : translate_tiled_kernel<TL, true, false>)
-                    : (rows ? translate_tiled_kernel<TL, false, true> : translate_tiled_kernel<TL, false, false>);
+    // accumulate mode: later groups of a target add at the L2 (double precision; red.f32 would
+    // flush subnormals) unless the caller asked for plain loads and stores ("accumulate_plain")
+    const int mode = !acc ? ACC_NONE : ((a.acc_plain || sizeof(Real) == 4) ? ACC_PLAIN : ACC_L2ADD);
+    auto kern = translate_tiled_kernel<TL, ACC_NONE, false>;
+    if (mode == ACC_NONE) kern = rows ? translate_tiled_kernel<TL, ACC_NONE, true> : translate_tiled_kernel<TL, ACC_NONE, false>;
+    else if (mode == ACC_PLAIN) kern = rows ? translate_tiled_kernel<TL, ACC_PLAIN, true> : translate_tiled_kernel<TL, ACC_PLAIN, false>;
+    else kern = rows ? translate_tiled_kernel<TL, ACC_L2ADD, true> : translate_tiled_kernel<TL, ACC_L2ADD, false>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;

@@ -109,6 +109,7 @@ struct sfmm_handle {
     std::vector<Pending> pending;
     int variant = 0;
     int64_t level_slab_pairs = 1 << 18;   // sfmm_m2l_level_host pipelines from 4 x this many pairs
+    bool accumulate_plain = false;        // "accumulate_plain" option (sfmm_m2l_accumulate*)
     long long* d_phase_clocks = nullptr;  // set by the "phase_clocks" option
 };
 
@@ -547,6 +548,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
         a.out = d_out;
         a.out_stride = out_stride;
         a.grp_target = plan->d_grp_target;
+        a.acc_plain = h->accumulate_plain;
         a.grp_ptr = plan->d_grp_ptr;
         a.n_targets = plan->n_targets;
         cudaError_t e = launch_zero_unwritten<Real>(plan->d_grp_ptr, plan->n_targets, p_out, d_out,
@@ -895,6 +897,10 @@ sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
     if (std::strcmp(name, "level_slab_pairs") == 0) {
         if (value < 64) return fail(SFMM_INVALID_ARGUMENT, "level_slab_pairs must be >= 64");
         h->level_slab_pairs = value;
+        return SFMM_OK;
+    }
+    if (std::strcmp(name, "accumulate_plain") == 0) {
+        h->accumulate_plain = value != 0;
         return SFMM_OK;
     }
     if (std::strcmp(name, "kernel_variant") == 0) {

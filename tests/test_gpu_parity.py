@@ -301,6 +301,32 @@ def test_resident_accumulation_layouts(oracle, h64, h32):
     assert h64.rows_len(20) == 440 and h64.rows_len(1) == 4
 
 
+def test_accumulate_plain_option_gives_the_same_bits(oracle, h64):
+    """The two ways the tiled kernel adds the groups of a target ("accumulate_plain" option:
+    L2 add by the single owner | load-add-store) against the documented tree, targets with one
+    to four groups, p_in != p_out included."""
+    rng = np.random.default_rng(313)
+    ns = 50
+    counts = np.array([1, 64, 65, 128, 129, 189, 200, 256, 0, 70] * 40)
+    tgt_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    idx = rng.integers(0, ns, int(tgt_ptr[-1])).astype(np.int32)
+    sh = random_shifts(rng, len(idx), with_axes=False)
+    for p_in, p_out in ((9, 9), (6, 11)):
+        src = random_solids(rng, ns, p_in)
+        _, per_pair = oracle.translate("m2l", p_in, p_out, src[idx], sh)
+        want = sharding.accumulation_tree(per_pair, tgt_ptr, 64)
+        plan = h64.plan(tgt_ptr, idx, sh, ns)
+        h64.set_option("kernel_variant", TILED)
+        try:
+            for plain in (0, 1):
+                h64.set_option("accumulate_plain", plain)
+                assert bits_equal(plan.accumulate_host(p_in, p_out, src), want), (p_in, p_out, plain)
+        finally:
+            h64.set_option("accumulate_plain", 0)
+            h64.set_option("kernel_variant", 0)
+        plan.close()
+
+
 def test_accumulation_mixed_orders(oracle, h64):
     """Target-owned accumulation with p_in != p_out (rows that only phase A or only phases
     C/D touch), both kernels, against the per-pair oracle results summed in the library's
