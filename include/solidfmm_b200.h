@@ -254,7 +254,15 @@ int sfmm_accumulation_unit(const sfmm_handle* h, int p_in, int p_out);
  * so every sum has one owner at a time and the order is fixed): 0 (default) = the owner sends
  * the sums of the later groups to the L2 to be added there (red.global.add.f64, no round
  * trip); 1 = the owner loads, adds and stores (no atomic or reduction instruction anywhere;
- * 4 % slower on the P = 20 level). Same bits either way. Single precision always uses 1. */
+ * 4 % slower on the P = 20 level). Same bits either way. Single precision always uses 1.
+ * "precise" (double precision handles): 1 = every swap pass on local-side data (the backward
+ * pass of M2L, both passes of L2L) carries its state in double-double, from cos(beta) = z / |r| through the recurrence, both transposed
+ * swap products and the rotation between them, and rounds once at the end. This removes the
+ * rounding floor of the rotation-based algorithm at high order (error against the O(P^4)
+ * sum `m2l_naive`: 2e-11 -> 3e-14 at P = 20, 1e-10 -> 3e-14 at P = 24; L2L gains 3x; the reference itself
+ * has the floor, so results then DIFFER from the reference's by that floor). Served by the
+ * generic kernel (every order, about a tenth of the tuned kernels' speed); combining it with
+ * another "kernel_variant" is INVALID_ARGUMENT at call time. No reference counterpart. */
 sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value);
 
 /* Measures the FMA-pipe peak (TFLOP/s, 2 flops per FMA) of the handle's device

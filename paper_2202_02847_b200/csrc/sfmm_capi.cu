@@ -110,6 +110,7 @@ struct sfmm_handle {
     int variant = 0;
     int64_t level_slab_pairs = 1 << 18;   // sfmm_m2l_level_host pipelines from 4 x this many pairs
     bool accumulate_plain = false;        // "accumulate_plain" option (sfmm_m2l_accumulate*)
+    bool precise = false;                 // "precise" option: double-double backward pass
     long long* d_phase_clocks = nullptr;  // set by the "phase_clocks" option
 };
 
@@ -202,6 +203,8 @@ sfmm_status check_orders(const sfmm_handle* h, int kind, int p_in, int p_out) {
         return fail(SFMM_INVALID_ARGUMENT, "mma kernel variant: double precision, handle order <= 30");
     if (h->variant == 4 && (p_in != p_out || p_in > 8))
         return fail(SFMM_INVALID_ARGUMENT, "small kernel variant: same order, at most 8");
+    if (h->precise && h->variant > 1)
+        return fail(SFMM_INVALID_ARGUMENT, "the precise mode runs on the generic kernel only (kernel_variant 0 or 1)");
     if (kind < 0 || kind > 2) return fail(SFMM_INVALID_ARGUMENT, "unknown translation kind");
     // pipeline.cpp:285-295
     if (p_in < 1 || p_out < 1)
@@ -269,6 +272,7 @@ sfmm_status translate_soa_impl(sfmm_handle* h, int kind, int64_t n, int p_in, in
     a.out_stride = out_stride;
     a.fail_flag = d_flag;
     a.variant = h->variant;
+    a.precise = h->precise;
     a.phase_clocks = h->d_phase_clocks;
     LaunchInfo info;
     cudaError_t e = launch_translate<Real>(tables_of<Real>(h), a, h->sm_count, stream, &info);
@@ -526,6 +530,7 @@ sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int
     a.p_in = p_in;
     a.p_out = p_out;
     a.variant = h->variant;
+    a.precise = h->precise;
     a.src_index = plan->d_src_index;  // accumulate mode decides which kernels apply
     a.in_layout = src_layout;
     if (translate_variant<Real>(tables_of<Real>(h), a) == 0)
@@ -861,12 +866,12 @@ int sfmm_accumulation_unit(const sfmm_handle* h, int p_in, int p_out) {
     if (!h || p_in < 1 || p_out < 1 || std::max(p_in, p_out) > h->order) return 0;
     if (h->precision == SFMM_F64) {
         TranslateArgs<double> a;
-        a.kind = KIND_M2L, a.p_in = p_in, a.p_out = p_out, a.variant = h->variant;
+        a.kind = KIND_M2L, a.p_in = p_in, a.p_out = p_out, a.variant = h->variant, a.precise = h->precise;
         a.src_index = h->d_flags;  // any non-null pointer: accumulate mode (never dereferenced)
         return translate_group_size<double>(h->td, a);
     }
     TranslateArgs<float> a;
-    a.kind = KIND_M2L, a.p_in = p_in, a.p_out = p_out, a.variant = h->variant;
+    a.kind = KIND_M2L, a.p_in = p_in, a.p_out = p_out, a.variant = h->variant, a.precise = h->precise;
     a.src_index = h->d_flags;
     return translate_group_size<float>(h->tf, a);
 }
@@ -897,6 +902,12 @@ sfmm_status sfmm_set_option(sfmm_handle* h, const char* name, int64_t value) {
     if (std::strcmp(name, "level_slab_pairs") == 0) {
         if (value < 64) return fail(SFMM_INVALID_ARGUMENT, "level_slab_pairs must be >= 64");
         h->level_slab_pairs = value;
+        return SFMM_OK;
+    }
+    if (std::strcmp(name, "precise") == 0) {
+        if (value && h->precision != SFMM_F64)
+            return fail(SFMM_INVALID_ARGUMENT, "the precise mode is double precision only");
+        h->precise = value != 0;
         return SFMM_OK;
     }
     if (std::strcmp(name, "accumulate_plain") == 0) {

@@ -67,6 +67,7 @@ struct TranslateArgs {
     const int64_t* grp_ptr = nullptr;     // [n_targets + 1] first group of every target
     int64_t n_targets = 0;
     bool acc_plain = false;              // direct form: load-add-store instead of the L2 add
+    bool precise = false;                // double-double backward pass (generic kernel, f64)
     const int* fail_flag = nullptr;      // device int; non-zero -> kernel writes nothing
     int variant = 0;                     // 0 auto, 1 generic, 2 tiled, 3 mma, 4 small-order kernel
     long long* phase_clocks = nullptr;   // optional [8] cycle counters of CTA 0 (tuning aid)

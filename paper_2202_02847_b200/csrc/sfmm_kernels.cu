@@ -447,6 +447,7 @@ int translate_variant(const DeviceTables<Real>& t, const TranslateArgs<Real>& a)
     const int p_rot = std::max(a.p_in, a.p_out);
     const bool mma = mma_ok(t, a), tiled = tiled_supports(a);
     const bool small = small_supports(a);
+    if (a.precise) return sizeof(Real) == 8 && a.variant <= 1 ? 1 : 0;  // generic kernel only
     switch (a.variant) {
         case 1: return 1;
         case 2: return tiled ? 2 : 0;
@@ -478,7 +479,7 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
     const int64_t n_groups = (a.n + kLanes - 1) / kLanes;
     const int limit = smem_optin_limit();
 
-    GenericLayout<Real> lay{p_rot, 8, true};
+    GenericLayout<Real> lay{p_rot, 8, true, a.precise};
     if ((int64_t)lay.smem_bytes() > limit) lay.warps = 4;
     if ((int64_t)lay.smem_bytes() > limit) {
         lay.warps = 8;
@@ -489,6 +490,11 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
 
     auto kern = lay.buf_in_smem ? translate_generic_kernel<Real, true>
                                 : translate_generic_kernel<Real, false>;
+    if constexpr (sizeof(Real) == 8) {
+        if (a.precise)
+            kern = lay.buf_in_smem ? translate_generic_kernel<Real, true, true>
+                                   : translate_generic_kernel<Real, false, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -511,7 +517,7 @@ cudaError_t launch_translate(const DeviceTables<Real>& t, const TranslateArgs<Re
         info->block = block;
         info->smem = smem;
         info->launches = 1;
-        info->variant = lay.buf_in_smem ? "generic/smem" : "generic/global-scratch";
+        info->variant = a.precise ? "generic/precise" : (lay.buf_in_smem ? "generic/smem" : "generic/global-scratch");
     }
     return e;
 }

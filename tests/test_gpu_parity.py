@@ -518,6 +518,56 @@ def test_level_from_particles_to_potentials(oracle, h64):
     assert worst < 2e-3   # order-10 truncation at the interaction-list separation
 
 
+def test_precise_mode_removes_the_rounding_floor(oracle, h64, h32):
+    """"precise" option: double-double backward pass. At P = 20 / 24 the default
+    result has the algorithm's floor against the O(P^4) sum (the reference's own, 1e-11 / 1e-10);
+    the precise result is within 2e-13. L2L: a there-and-back pair returns to the input at
+    least twice as close (its state is rounded to double between the passes and in the z-step). M2M and the accumulate path run too;
+    single precision refuses the option."""
+    rng = np.random.default_rng(557)
+    try:
+        for p, floor in ((8, 0.0), (20, 1e-12), (24, 1e-11)):
+            src, sh = workloads.config0(70 + p, 48, p)
+            naive = oracle.m2l_naive(p, p, src, sh)[1]
+            h64.set_option("precise", 0)
+            plain = h64.translate_host(capi.M2L, p, p, src, sh)
+            h64.set_option("precise", 1)
+            prec = h64.translate_host(capi.M2L, p, p, src, sh)
+            e_plain, e_prec = normalized_error(plain, naive), normalized_error(prec, naive)
+            assert e_prec < 2e-13, (p, e_prec)
+            assert e_plain > floor and e_prec <= e_plain * 1.5 + 1e-15, (p, e_plain, e_prec)
+            # mixed orders and in accumulate mode
+            out = h64.translate_host(capi.M2L, p, max(1, p - 5), src, sh)
+            assert normalized_error(out, oracle.m2l_naive(p, max(1, p - 5), src, sh)[1]) < 2e-13
+        p = 20
+        src, sh = workloads.config0(91, 32, p)
+        _, sh2 = workloads.config1(92, 32, p)
+        loc = h64.translate_host(capi.M2L, p, p, src, sh)
+        back_prec = h64.translate_host(capi.L2L, p, p, h64.translate_host(capi.L2L, p, p, loc, sh2), -sh2)
+        h64.set_option("precise", 0)
+        back = h64.translate_host(capi.L2L, p, p, h64.translate_host(capi.L2L, p, p, loc, sh2), -sh2)
+        assert normalized_error(back_prec, loc) < 0.5 * normalized_error(back, loc)
+        # M2M is untouched by the option (multipole-side backward pass): same bits
+        m_plain = h64.translate_host(capi.M2M, p, p, src, sh2)
+        h64.set_option("precise", 1)
+        assert bits_equal(h64.translate_host(capi.M2M, p, p, src, sh2), m_plain)
+        tgt_ptr = np.array([0, 3, 3, 32], np.int64)
+        plan = h64.plan(tgt_ptr, np.arange(32, dtype=np.int32), sh, 32)
+        acc = plan.accumulate_host(p, p, src)
+        plan.close()
+        per_pair = h64.translate_host(capi.M2L, p, p, src, sh)
+        want = sharding.accumulation_tree(per_pair, tgt_ptr, h64.accumulation_unit(p, p))
+        assert bits_equal(acc, want)
+        with pytest.raises(capi.InvalidArgument):
+            h32.set_option("precise", 1)
+        h64.set_option("kernel_variant", TILED)
+        with pytest.raises(capi.InvalidArgument):
+            h64.translate_host(capi.M2L, 8, 8, src[:, :72], sh)
+    finally:
+        h64.set_option("kernel_variant", 0)
+        h64.set_option("precise", 0)
+
+
 # ---- API contracts ---------------------------------------------------------
 
 def test_error_contracts(h64):
