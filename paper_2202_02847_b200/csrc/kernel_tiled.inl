@@ -651,10 +651,11 @@ __device__ __forceinline__ void add_ordered(float* dst, float v) { __stcg(dst, _
 
 // ROWS: the sources are in LAYOUT_ROWS (sfmm_internal.hpp): a lane reads re, im of two
 // consecutive m of its own source with one load and touches whole sectors only.
-template <int TL, int ACC, bool ROWS>
+template <int TL, int ACC, bool ROWS, int CHA>
 __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int gen, int flags) {
     constexpr int L = 32 * TL;
-    constexpr int CHA = ROWS ? 2 : 4;  // elements per batch of phase-A loads (streamed SoA inputs come from HBM: larger batches)
+    // CHA: elements per batch of phase-A loads (2; 4 for streamed SoA inputs at the orders where
+    // it was measured to pay, launch_translate_tiled)
     const int lane = threadIdx.x & 31;
     const int misc_off = flags >> ROWS_MISC_SHIFT;  // bytes: {mbarrier, counters, row_done, RowConst}
     int* counters = reinterpret_cast<int*>(smem_raw + misc_off + 8);
@@ -882,7 +883,7 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
     }
 }
 
-template <int TL, int ACC, bool ROWS>
+template <int TL, int ACC, bool ROWS, int CHA = 2>
 __global__ void __launch_bounds__(SFMM_MAXTHREADS, 1)
 translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, int p_rot,
                        int tab_len) {
@@ -1022,7 +1023,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         }
         // ---- D of `cur`, A of `nxt`
         if (cur >= 0 || has_next)
-            elementwise_rows<TL, ACC, ROWS>(
+            elementwise_rows<TL, ACC, ROWS, CHA>(
                 cur, nxt, gen,
                 rows_misc | (cur >= 0 ? ROWS_D : 0) | (has_next ? ROWS_A : 0) |
                     (parity ? ROWS_PARITY_A : ROWS_PARITY_D));
@@ -1201,7 +1202,12 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     // flush subnormals) unless the caller asked for plain loads and stores ("accumulate_plain")
     const int mode = !acc ? ACC_NONE : ((a.acc_plain || sizeof(Real) == 4) ? ACC_PLAIN : ACC_L2ADD);
     auto kern = translate_tiled_kernel<TL, ACC_NONE, false>;
-    if (mode == ACC_NONE) kern = rows ? translate_tiled_kernel<TL, ACC_NONE, true> : translate_tiled_kernel<TL, ACC_NONE, false>;
+    // streamed SoA inputs: four-element load batches in phase A where 12 warps run one group per
+    // SM (measured: P = 16 +8 %; P = 12 -3 %, 14 -8 %, 20 -3 % with two CTAs per SM or a full SM)
+    const bool wide = sizeof(Real) == 8 && p_rot >= 15 && p_rot <= 18;
+    if (mode == ACC_NONE)
+        kern = rows ? translate_tiled_kernel<TL, ACC_NONE, true>
+                    : (wide ? translate_tiled_kernel<TL, ACC_NONE, false, 4> : translate_tiled_kernel<TL, ACC_NONE, false>);
     else if (mode == ACC_PLAIN) kern = rows ? translate_tiled_kernel<TL, ACC_PLAIN, true> : translate_tiled_kernel<TL, ACC_PLAIN, false>;
     else kern = rows ? translate_tiled_kernel<TL, ACC_L2ADD, true> : translate_tiled_kernel<TL, ACC_L2ADD, false>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
