@@ -1216,7 +1216,8 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-    const int grid = (int)std::min<int64_t>(n_groups, (int64_t)sm_count * per_sm);
+    const int sms = std::max(1, sm_count - std::max(0, a.reserve_sms));
+    const int grid = (int)std::min<int64_t>(n_groups, (int64_t)sms * per_sm);
 
     TiledTables tt;
     tt.stream[0] = t.stream[0];

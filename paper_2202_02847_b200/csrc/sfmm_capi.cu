@@ -523,9 +523,10 @@ sfmm_status plan_create_impl(sfmm_handle* h, int64_t n_targets, const int64_t* t
 template <typename Real>
 sfmm_status accumulate_impl(sfmm_handle* h, const sfmm_plan* plan, int p_in, int p_out,
                             const Real* d_src, int64_t src_stride, int src_layout, Real* d_out,
-                            int64_t out_stride, cudaStream_t stream) {
+                            int64_t out_stride, cudaStream_t stream, int reserve_sms = 0) {
     const int64_t so = solid_len(p_out);
     TranslateArgs<Real> a;
+    a.reserve_sms = reserve_sms;
     a.kind = KIND_M2L;
     a.p_in = p_in;
     a.p_out = p_out;
@@ -683,16 +684,39 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
     CU(d_src.alloc(es * srows * n_sources));
     CU(d_flags.alloc(sizeof(int) * 2 * K));
     CU(cudaMemsetAsync(d_flags.p, 0, sizeof(int) * 2 * K, sc));
-    CU(cudaMemcpyAsync(d_src_aos.p, src_aos, es * si * n_sources, cudaMemcpyHostToDevice, sc));
-    CU(launch_pack_rows<Real>(d_src_aos.as<Real>(), d_src.as<Real>(), n_sources, p_in, sc));
-    CU(cudaEventRecord(ev_src, sc));
-    CU(cudaStreamWaitEvent(sx, ev_src, 0));
-    h->launches += 1;
+    // The sources go up in chunks, interleaved with the pair lists on the copy stream: a slab's
+    // kernels wait (through its `ready` event, recorded behind them) only for the chunks that
+    // hold the sources its pairs name, so the first slab starts after a part of the upload
+    // (a level sorted by box index: about a third) instead of all of it. Chunks no slab names
+    // are never sent.
+    constexpr int kSrcChunks = 8;
+    const int64_t chunk_len = (n_sources + kSrcChunks - 1) / kSrcChunks;
+    int chunks_queued = 0;
+    auto queue_sources_upto = [&](int64_t last_source) -> cudaError_t {
+        const int need = chunk_len > 0 ? (int)std::min<int64_t>(last_source / chunk_len, kSrcChunks - 1) : -1;
+        for (; chunks_queued <= need; ++chunks_queued) {
+            const int64_t c0 = chunks_queued * chunk_len, c1 = std::min(n_sources, c0 + chunk_len);
+            if (c1 <= c0) continue;
+            cudaError_t e = cudaMemcpyAsync(d_src_aos.as<Real>() + c0 * si, src_aos + c0 * si, es * si * (c1 - c0),
+                                            cudaMemcpyHostToDevice, sc);
+            if (e == cudaSuccess)
+                e = launch_pack_rows<Real>(d_src_aos.as<Real>() + c0 * si, d_src.as<Real>() + c0 * srows, c1 - c0,
+                                           p_in, sc);
+            if (e != cudaSuccess) return e;
+            h->launches += 1;
+        }
+        return cudaSuccess;
+    };
     for (int k = 0; k < K; ++k) {
         slabs.emplace_back(new Slab(sc, sx));
         Slab& S = *slabs.back();
         const int64_t t0 = cut[k], t1 = cut[k + 1], nt = t1 - t0;
         const int64_t p0 = tgt_ptr[t0], np = tgt_ptr[t1] - p0;
+        {  // highest valid source index of the slab (invalid ones are reported by the plan kernel)
+            int32_t hi = -1;
+            for (int64_t j = p0; j < p0 + np; ++j) hi = std::max(hi, src_index[j]);
+            if (hi >= 0) CU(queue_sources_upto(std::min<int64_t>(hi, n_sources - 1)));
+        }
         S.t0 = t0;
         S.ostride = round_up32(std::max<int64_t>(nt, 1));
         S.grp_ptr.assign((size_t)nt + 1, 0);
@@ -742,8 +766,11 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
         CU(cudaEventRecord(S.ready, sc));
         // compute of the slab on the second stream
         CU(cudaStreamWaitEvent(sx, S.ready, 0));
+        // one SM stays free of the persistent translation kernel: the small kernels of the
+        // following slabs (plan building, source packing) run there beside it instead of
+        // waiting for it to end, which would stall the copy stream behind them
         const sfmm_status st = accumulate_impl<Real>(h, &P, p_in, p_out, d_src.as<Real>(), srows, LAYOUT_ROWS,
-                                                     S.out.as<Real>(), S.ostride, sx);
+                                                     S.out.as<Real>(), S.ostride, sx, /*reserve_sms=*/1);
         if (st != SFMM_OK) return st;
         CU(launch_unpack_soa<Real>(S.out.as<Real>(), S.out_aos.as<Real>(), nt, p_out, S.ostride, sx));
         h->launches += 1;

@@ -68,6 +68,7 @@ struct TranslateArgs {
     int64_t n_targets = 0;
     bool acc_plain = false;              // direct form: load-add-store instead of the L2 add
     bool precise = false;                // double-double backward pass (generic kernel, f64)
+    int reserve_sms = 0;                 // tiled kernel: SMs left free for concurrent small kernels
     const int* fail_flag = nullptr;      // device int; non-zero -> kernel writes nothing
     int variant = 0;                     // 0 auto, 1 generic, 2 tiled, 3 mma, 4 small-order kernel
     long long* phase_clocks = nullptr;   // optional [8] cycle counters of CTA 0 (tuning aid)
