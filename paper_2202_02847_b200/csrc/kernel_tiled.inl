@@ -450,7 +450,7 @@ struct TiledLayout {
     // triangle, staged stream, {mbarrier, task counters} (32 bytes), per-row completion
     // counters of the backward swap pass, launch constants of the row function
     __host__ __device__ size_t smem_bytes() const {
-        return sizeof(Real) * (buf_elems() + tab_len) + 32 + sizeof(int) * ((PMAX + 3) / 4 * 4) +
+        return sizeof(Real) * (buf_elems() + tab_len) + 32 + 2 * sizeof(int) * ((PMAX + 3) / 4 * 4) +
                128;  // RowConst
     }
 };
@@ -614,7 +614,8 @@ struct RowConst {
 };
 // per-call flags of elementwise_rows
 enum : int { ROWS_D = 1, ROWS_A = 2, ROWS_PARITY_D = 4, ROWS_PARITY_A = 8, ROWS_MISC_SHIFT = 4 };
-constexpr int ROW_DONE_BYTES = sizeof(int) * ((PMAX + 3) / 4 * 4);
+constexpr int ROW_DONE_INTS = (PMAX + 3) / 4 * 4;
+constexpr int ROW_DONE_BYTES = 2 * sizeof(int) * ROW_DONE_INTS;  // row_done, row_a_done
 
 // Phases D and A, row by row (reference pipeline.cpp:251-257 and :148-154):
 //   D (group g):   rotate by -alpha, scale by the row factor, then store (ACC = false)
@@ -660,6 +661,7 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
     const int misc_off = flags >> ROWS_MISC_SHIFT;  // bytes: {mbarrier, counters, row_done, RowConst}
     int* counters = reinterpret_cast<int*>(smem_raw + misc_off + 8);
     const int* row_done = counters + 6;
+    int* row_a_done = counters + 6 + ROW_DONE_INTS;  // phase A of row n finished (value: trip + 1)
     const RowConst& e = *reinterpret_cast<const RowConst*>(smem_raw + misc_off + 32 + ROW_DONE_BYTES);
     const int p_rot = e.p_rot;
     const int i1 = min(1, p_rot - 1);  // row of cos/sin(alpha) in the tables
@@ -880,6 +882,12 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
             if (m0 > n) break;
             issue(m0);
         }
+        // row n of `nxt` is in place: its forward swap passes may start (translate_tiled_kernel)
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            *reinterpret_cast<volatile int*>(&row_a_done[n]) = gen + 1;
+        }
     }
 }
 
@@ -919,7 +927,8 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     }
     bool tab_pending = true;  // a bulk copy is in flight that the next swap phase must wait for
     if (threadIdx.x < 6) counters[threadIdx.x] = 0;
-    if (threadIdx.x < PMAX) row_done[threadIdx.x] = 0;
+    int* row_a_done = row_done + ROW_DONE_INTS;        // [PMAX] trip + 1 of the last finished phase A per row
+    if (threadIdx.x < PMAX) row_done[threadIdx.x] = row_a_done[threadIdx.x] = 0;
 
     // per-phase cycle counters of CTA 0 (tuning aid, tools/perf_probe.py PHASES=1): compiled in
     // only with -DSFMM_PHASE_CLOCKS, because the running time stamp costs every warp a
@@ -1039,22 +1048,25 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
             tab_phase ^= 1;
             tab_pending = false;
         }
-        __syncthreads();  // phase A of `nxt` and its operator stream are in place
         SFMM_PHASE_MARK(1)
-        if (threadIdx.x == 0) counters[2] = counters[3] = counters[4] = 0;
 
-        // ---- B: forward swap passes, largest rows first
+        // ---- B: forward swap passes, largest rows first. No CTA barrier in front: a half task
+        // waits for phase A of ITS row (row_a_done), so the multiplications of the rows that
+        // are in place fill the latency-bound tail of the row phase. (Every row task has been
+        // taken by a warp before any warp arrives here, so the wait cannot deadlock.)
         {
             Ctx<TL> c{(int)lay.tab_len, 0, gv.cb, gv.sb, src_local};
             for (int task = fetch_task(&counters[0], lane); task < 2 * p_in;
                  task = fetch_task(&counters[0], lane)) {
                 const int n = p_in - 1 - (task >> 1);
+                while (ld_volatile_shared(&row_a_done[n]) != gen) __nanosleep(32);
+                __threadfence_block();
                 half_task_dispatch<TL>(c, n, task & 1, n);
             }
         }
         __syncthreads();
         SFMM_PHASE_MARK(2)
-        if (threadIdx.x == 0) counters[0] = 0;
+        if (threadIdx.x == 0) counters[0] = counters[2] = counters[3] = counters[4] = 0;
         if (two_sides) {  // stage the backward-side stream while the z-step runs
             if (threadIdx.x == 0) bulk_load(tab, tt.stream[side_bwd], tt.bytes[1], mbar);
             tab_pending = true;
