@@ -995,15 +995,16 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         geometry_phase<TL>(a, g_first, p_rot, geo_base, src_local, dst_local, warp, lane);
     __syncthreads();
 
-    // Schedule (three CTA-wide barriers per group). One trip of the loop:
+    // Schedule (two CTA-wide barriers per group). One trip of the loop:
     //   CDA  of the group `cur` that has finished its z-step (none in the first trip):
     //        backward swap passes (C) on most warps; the other warps, and every warp that
     //        finds the C queue empty, take rows from a second queue: phase D of `cur` and
     //        phase A of `nxt` on a row whose two C half tasks are done (row_done). The
     //        latency-bound elementwise work so runs beside the multiplications;
-    //   B    of `nxt`: forward swap passes, one half task per (row, parity class);
-    //   Z    of `nxt`: z-axis step per (column, re | im); the first TL warps first prepare
-    //        the geometry of the group after it.
+    //   B    of `nxt`: forward swap passes, one half task per (row, parity class), each behind
+    //        phase A of its own row (row_a_done), no barrier in front;
+    //   Z    of `nxt` (barriers on both sides): z-axis step per (column, re | im); the first TL
+    //        warps first prepare the geometry of the group after it.
     // The row code is inline at this one place (out of line, called directly, ptxas fits
     // caller and callee into one register budget and spills the loads in flight).
     int parity = 0, gen = 0;  // parity: geometry buffer of `nxt`
