@@ -1156,11 +1156,12 @@ cudaError_t ensure_constants() {
     return cudaSuccess;
 }
 
-int tiled_row_warps_for(int warps) {
+int tiled_row_warps_for(int warps, bool gathered) {
     if (const char* env = getenv("SFMM_TILED_ROW_WARPS")) return atoi(env);
-    // measured: no dedicated row warps; every warp takes rows when the C queue is empty
-    (void)warps;
-    return 0;
+    // measured with the two-barrier schedule (level, P = 20: 0 / 2 / 4 row warps 5.77 / 5.73 /
+    // 5.73 ms; batched P = 16: 1.036 / 1.045 / 1.068 ms): two warps start the last phase in the
+    // row queue where the sources are gathered (the gathers are in flight early), none otherwise
+    return gathered && warps >= 8 ? 2 : 0;
 }
 
 int tiled_prefetch_for(int p_rot) {
@@ -1237,7 +1238,7 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     tt.stream[1] = t.stream[1];
     tt.bytes[0] = (uint32_t)(staged(a.p_in) * sizeof(Real));
     tt.bytes[1] = (uint32_t)(staged(a.p_out) * sizeof(Real));
-    tt.row_warps = tiled_row_warps_for(block / 32);
+    tt.row_warps = tiled_row_warps_for(block / 32, acc && rows);
     tt.prefetch = tiled_prefetch_for(p_rot);
     e = cudaMallocAsync((void**)&tt.scratch, sizeof(Real) * (size_t)grid * 2 * geo_elems<TL>(p_rot), stream);
     if (e != cudaSuccess) return e;
