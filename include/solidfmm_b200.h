@@ -145,8 +145,9 @@ sfmm_status sfmm_pack_rows(sfmm_handle* h, int64_t n, int p, const void* d_aos,
  * potential of the local expansion of box point_box[i] (NULL: box i) at points[i][3].
  * Results equal the reference's (parity build, -mfma -ffp-contract=fast) bit for bit, charges and
  * sums taken in the reference's order. Device entry points take device pointers and a stream;
- * the _host forms take host arrays (expansions in the AoS layout). Orders up to
- * sfmm_harmonics_max_order() (32). */
+ * the _host forms take host arrays (expansions in the AoS layout) and validate the box
+ * indices (INVALID_ARGUMENT); the device form writes NaN for a point whose box index is out
+ * of range. Orders up to sfmm_harmonics_max_order() (32). */
 enum { SFMM_LAYOUT_SOA = 0, SFMM_LAYOUT_ROWS = 1, SFMM_LAYOUT_AOS = 2 };
 int sfmm_harmonics_max_order(void);
 sfmm_status sfmm_p2m(sfmm_handle* h, int64_t n_boxes, const int64_t* d_box_ptr,
@@ -245,7 +246,8 @@ sfmm_status sfmm_level_pairs(int nx, int ny, int nz, int halo, double box_size,
  * reference has no accumulate mode, pipeline.cpp:258-265 overwrites.) */
 int sfmm_accumulation_unit(const sfmm_handle* h, int p_in, int p_out);
 
-/* Tuning knobs without a reference counterpart. "kernel_variant": 0 = automatic
+/* Options of a handle (set them before the handle is shared between threads: calls read them
+ * without locking). Tuning knobs without a reference counterpart. "kernel_variant": 0 = automatic
  * (default), 1 = generic kernel (any order), 2 = tiled kernel (orders <= 20
  * double / <= 18 single; INVALID_ARGUMENT at call time beyond that), 3 = FP64
  * tensor-core kernel (double precision, handle order <= 30), 4 = small-order kernel

@@ -249,8 +249,13 @@ eval_local_kernel(const int32_t* __restrict__ point_box, const Real* __restrict_
     int64_t cached = -1;
     for (int64_t base = i0; base < i1; base += per_warp) {
         const int64_t i = base + sub;
-        const bool on = lane_on && i < i1;
-        const int64_t b = on ? (point_box ? (int64_t)point_box[i] : i) : -1;
+        bool on = lane_on && i < i1;
+        int64_t b = on ? (point_box ? (int64_t)point_box[i] : i) : -1;
+        if (on && (b < 0 || b >= n_boxes)) {  // no such box: the point gets a NaN, nothing is read
+            if (l == 0) out[i] = (Real)__longlong_as_double(0x7ff8000000000000ll);
+            on = false;
+            b = -1;
+        }
         if (on && b != cached) {  // the lanes of a sub-group agree
             if (layout == LAYOUT_AOS) {
                 for (int c = l; c < S; c += half) my_loc[c] = locals[b * S + c];

@@ -479,6 +479,17 @@ def test_p2m_layouts_feed_the_translation_path(oracle, h64):
     loc = oracle.translate("m2l", p, p, want, sh)[1]
     phi = np.array([oracle.eval_local_fma(p, loc[b], lc[b], x[b]) for b in range(nb)])
     assert bits_equal(d_phi.cpu().numpy(), phi)
+    # device form, a point whose box index is out of range: NaN for that point, the rest untouched
+    pb = torch.arange(nb, dtype=torch.int32, device=dev)
+    pb[5] = nb + 3
+    pb[9] = -1
+    h64.eval_local(nb, pb.data_ptr(), d_x.data_ptr(), d_lc.data_ptr(), nb, p, capi.LAYOUT_SOA, d_loc.data_ptr(), stride,
+                   d_phi.data_ptr(), st)
+    torch.cuda.synchronize()
+    got = d_phi.cpu().numpy()
+    assert np.isnan(got[5]) and np.isnan(got[9])
+    ok = np.ones(nb, bool); ok[[5, 9]] = False
+    assert bits_equal(got[ok], phi[ok])
     direct = np.array([np.sum(ch[b * per:(b + 1) * per, 3] /
                               np.linalg.norm(x[b] - ch[b * per:(b + 1) * per, :3], axis=1)) for b in range(nb)])
     assert np.max(np.abs(phi - direct)) < 1e-6 * np.max(np.abs(direct))
