@@ -422,8 +422,8 @@ def main():
         d_src = torch.empty((n_src, handle.rows_len(20)), dtype=tdt, device=dev)
         handle.pack_rows(n_src, 20, d_src_aos.data_ptr(), d_src.data_ptr(), stream)
         d_out = torch.empty((S_out, ostride), dtype=tdt, device=dev)
-        excluded = ["sfmm_plan_create (pair list upload, padding, zero-shift scan and the per-pair "
-                    "hypot / division geometry of geometry.cpp:11-30: build_plan_kernel)",
+        excluded = ["sfmm_plan_create (pair list upload, padding, zero-shift scan, and the hypot / division "
+                    "geometry of geometry.cpp:11-30, once per distinct shift: build_plan_kernel, dedup_*_kernel)",
                     "sfmm_pack_rows (AoS -> rows layout of the sources)"]
 
         def step_resident():
