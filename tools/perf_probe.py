@@ -18,6 +18,8 @@ dev = torch.device("cuda", 0)
 h = capi.Handle(prec, P)
 import os as _os0
 h.set_option("kernel_variant", int(_os0.environ.get("VARIANT", "0")))
+if _os0.environ.get("PRECISE"):
+    h.set_option("precise", 1)
 peak = h.measure_fma_peak()
 S = P * (P + 1)
 stream = torch.cuda.current_stream().cuda_stream
