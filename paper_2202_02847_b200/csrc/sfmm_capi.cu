@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -689,7 +690,11 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
     // hold the sources its pairs name, so the first slab starts after a part of the upload
     // (a level sorted by box index: about a third) instead of all of it. Chunks no slab names
     // are never sent.
-    constexpr int kSrcChunks = 8;
+    static const int kSrcChunks = [] {
+        const char* env = std::getenv("SFMM_LEVEL_SRC_CHUNKS");  // tuning: 1 = all sources first
+        const int v = env ? std::atoi(env) : 8;
+        return v >= 1 && v <= 64 ? v : 8;
+    }();
     const int64_t chunk_len = (n_sources + kSrcChunks - 1) / kSrcChunks;
     int chunks_queued = 0;
     auto queue_sources_upto = [&](int64_t last_source) -> cudaError_t {
