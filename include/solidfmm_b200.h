@@ -147,7 +147,7 @@ sfmm_status sfmm_pack_rows(sfmm_handle* h, int64_t n, int p, const void* d_aos,
  * sums taken in the reference's order. Device entry points take device pointers and a stream;
  * the _host forms take host arrays (expansions in the AoS layout) and validate the box
  * indices (INVALID_ARGUMENT); the device form writes NaN for a point whose box index is out
- * of range. Orders up to sfmm_harmonics_max_order() (32). */
+ * of range. Every order of the handle (tuned kernels to order 32, plain ones above). */
 enum { SFMM_LAYOUT_SOA = 0, SFMM_LAYOUT_ROWS = 1, SFMM_LAYOUT_AOS = 2 };
 int sfmm_harmonics_max_order(void);
 sfmm_status sfmm_p2m(sfmm_handle* h, int64_t n_boxes, const int64_t* d_box_ptr,

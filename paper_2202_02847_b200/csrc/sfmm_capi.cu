@@ -1127,8 +1127,6 @@ sfmm_status sfmm_p2m(sfmm_handle* h, int64_t n_boxes, const int64_t* d_box_ptr, 
     if (!h || n_boxes < 0 || !harmonics_layout_ok(layout))
         return fail(SFMM_INVALID_ARGUMENT, "bad p2m arguments");
     if (order < 1 || order > h->order) return fail(SFMM_INVALID_ARGUMENT, "order out of range for this handle");
-    if (order > harmonics_max_order())
-        return fail(SFMM_INVALID_ARGUMENT, "p2m / eval_local on the device cover orders <= 32");
     if (n_boxes == 0) return SFMM_OK;
     if (!d_box_ptr || !d_charges || !d_centers || !d_out) return fail(SFMM_INVALID_ARGUMENT, "null pointer");
     if (layout == SFMM_LAYOUT_SOA && out_stride < n_boxes)
@@ -1151,8 +1149,6 @@ sfmm_status sfmm_eval_local(sfmm_handle* h, int64_t n_points, const int32_t* d_p
     if (!h || n_points < 0 || n_boxes < 0 || !harmonics_layout_ok(layout))
         return fail(SFMM_INVALID_ARGUMENT, "bad eval_local arguments");
     if (order < 1 || order > h->order) return fail(SFMM_INVALID_ARGUMENT, "order out of range for this handle");
-    if (order > harmonics_max_order())
-        return fail(SFMM_INVALID_ARGUMENT, "p2m / eval_local on the device cover orders <= 32");
     if (n_points == 0) return SFMM_OK;
     if (!d_points || !d_centers || !d_locals || !d_out) return fail(SFMM_INVALID_ARGUMENT, "null pointer");
     if (layout == SFMM_LAYOUT_SOA && stride < n_boxes)

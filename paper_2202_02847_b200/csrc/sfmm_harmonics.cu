@@ -26,7 +26,7 @@
 namespace sfmm {
 namespace {
 
-constexpr int kHarmMaxOrder = 32;  // lane = m
+constexpr int kHarmMaxOrder = 32;  // paired-column kernels (a warp serves whole boxes / points); plain kernels above
 
 template <typename Real>
 __device__ __forceinline__ Real real_min();
@@ -306,6 +306,99 @@ eval_local_kernel(const int32_t* __restrict__ point_box, const Real* __restrict_
     }
 }
 
+// ---- orders above 32 (the handle goes to 86 in double precision) ---------------------------
+// Same arithmetic and the same orders of summation, plain mapping: one warp per box / point,
+// lane = m, m + 32, m + 64; P2M accumulates in the output itself (a thread owns its
+// coefficients), L2P keeps the products in a shared triangle. Dynamic shared memory:
+// inv2n [P + 1] | L2P: terms [P(P+1)/2], rows [P] (one warp per block).
+template <typename Real>
+__global__ void __launch_bounds__(32)
+p2m_generic_kernel(const int64_t* __restrict__ box_ptr, const Real* __restrict__ charges,
+                   const Real* __restrict__ centers, int64_t n_boxes, int order, int layout,
+                   Real* __restrict__ out, int64_t stride) {
+    Real* inv2n = reinterpret_cast<Real*>(harm_smem);
+    for (int i = threadIdx.x; i <= order; i += 32) inv2n[i] = i ? Real(1) / Real(2 * i) : Real(0);
+    __syncwarp();
+    const int lane = threadIdx.x;
+    for (int64_t b = blockIdx.x; b < n_boxes; b += gridDim.x) {
+        const Real cx = centers[3 * b], cy = centers[3 * b + 1], cz = centers[3 * b + 2];
+        const int64_t j0 = box_ptr[b], j1 = box_ptr[b + 1];
+        for (int m = lane; m < order; m += 32) {
+            for (int n = m; n < order; ++n) {
+                out[out_index(layout, b, n, m, 0, order, stride)] = Real(0);
+                out[out_index(layout, b, n, m, 1, order, stride)] = Real(0);
+            }
+            for (int64_t j = j0; j < j1; ++j) {
+                ChargeState<Real> st;
+                st.start(charges[4 * j] - cx, charges[4 * j + 1] - cy, charges[4 * j + 2] - cz, charges[4 * j + 3], m,
+                         m, inv2n);
+                for (int n = m; n < order; ++n) {
+                    Real re, im;
+                    st.slot(n, m, n - m, false, n > m ? Real(1) / Real(n * n - m * m) : Real(0), re, im);
+                    const int64_t ir = out_index(layout, b, n, m, 0, order, stride);
+                    const int64_t ii = out_index(layout, b, n, m, 1, order, stride);
+                    out[ir] = fma_(st.q, re, out[ir]);
+                    out[ii] = fma_(st.q, im, out[ii]);
+                }
+            }
+        }
+        if (layout == LAYOUT_ROWS && lane == 0) {
+            for (int n = 0; n < order; ++n)
+                for (int k = 2 * (n + 1); k < rows_off(n + 1) - rows_off(n); ++k)
+                    out[b * rows_off(order) + rows_off(n) + k] = Real(0);
+        }
+    }
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(32)
+eval_local_generic_kernel(const int32_t* __restrict__ point_box, const Real* __restrict__ points,
+                          const Real* __restrict__ centers, int64_t n_points, int64_t n_boxes, int order,
+                          int layout, const Real* __restrict__ locals, int64_t stride, Real* __restrict__ out) {
+    Real* inv2n = reinterpret_cast<Real*>(harm_smem);
+    Real* terms = inv2n + order + 1;
+    Real* rows = terms + order * (order + 1) / 2;
+    for (int i = threadIdx.x; i <= order; i += 32) inv2n[i] = i ? Real(1) / Real(2 * i) : Real(0);
+    __syncwarp();
+    const int lane = threadIdx.x;
+    for (int64_t i = blockIdx.x; i < n_points; i += gridDim.x) {
+        const int64_t b = point_box ? (int64_t)point_box[i] : i;
+        if (b < 0 || b >= n_boxes) {
+            if (lane == 0) out[i] = (Real)__longlong_as_double(0x7ff8000000000000ll);
+            continue;
+        }
+        const Real x = points[3 * i] - centers[3 * b], y = points[3 * i + 1] - centers[3 * b + 1],
+                   z = points[3 * i + 2] - centers[3 * b + 2];
+        for (int m = lane; m < order; m += 32) {
+            ChargeState<Real> st;
+            st.start(x, y, z, Real(0), m, m, inv2n);
+            for (int n = m; n < order; ++n) {
+                Real vre, vim;
+                st.slot(n, m, n - m, false, n > m ? Real(1) / Real(n * n - m * m) : Real(0), vre, vim);
+                const Real lre = locals[out_index(layout, b, n, m, 0, order, stride)];
+                const Real lim = locals[out_index(layout, b, n, m, 1, order, stride)];
+                terms[n * (n + 1) / 2 + m] = m == 0 ? vre : fma_(lre, vre, lim * vim);
+            }
+        }
+        __syncwarp();
+        for (int n = lane; n < order; n += 32) {
+            Real rowsum = Real(0);
+            for (int k = 1; k <= n; ++k) rowsum = rowsum + terms[n * (n + 1) / 2 + k];
+            rows[n] = rowsum;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            Real total = Real(0);
+            for (int n = 0; n < order; ++n) {
+                total = fma_(locals[out_index(layout, b, n, 0, 0, order, stride)], terms[n * (n + 1) / 2], total);
+                total = total + (rows[n] + rows[n]);
+            }
+            out[i] = total;
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 template <typename Real>
@@ -313,7 +406,13 @@ cudaError_t launch_p2m(const int64_t* box_ptr, const Real* charges, const Real* 
                        int64_t n_boxes, int order, int layout, Real* out, int64_t stride,
                        cudaStream_t stream) {
     if (n_boxes <= 0) return cudaSuccess;
-    if (order > kHarmMaxOrder) return cudaErrorInvalidValue;
+    if (order > kHarmMaxOrder) {
+        const size_t smem = sizeof(Real) * (order + 1);
+        const unsigned blocks = (unsigned)std::min<int64_t>(n_boxes, 148 * 32);
+        p2m_generic_kernel<Real><<<blocks, 32, smem, stream>>>(box_ptr, charges, centers, n_boxes, order, layout, out,
+                                                               stride);
+        return cudaGetLastError();
+    }
     const int per_warp = 32 / ((order + 1) / 2);
     const int64_t warps = (n_boxes + per_warp - 1) / per_warp;
     const unsigned grid = (unsigned)((warps + 3) / 4);
@@ -335,7 +434,13 @@ cudaError_t launch_eval_local(const int32_t* point_box, const Real* points, cons
                               int64_t n_points, int64_t n_boxes, int order, int layout,
                               const Real* locals, int64_t stride, Real* out, cudaStream_t stream) {
     if (n_points <= 0) return cudaSuccess;
-    if (order > kHarmMaxOrder) return cudaErrorInvalidValue;
+    if (order > kHarmMaxOrder) {
+        const size_t smem = sizeof(Real) * ((size_t)order + 1 + (size_t)order * (order + 1) / 2 + order);
+        const unsigned blocks = (unsigned)std::min<int64_t>(n_points, 148 * 8);
+        eval_local_generic_kernel<Real><<<blocks, 32, smem, stream>>>(point_box, points, centers, n_points, n_boxes,
+                                                                      order, layout, locals, stride, out);
+        return cudaGetLastError();
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -353,7 +458,7 @@ cudaError_t launch_eval_local(const int32_t* point_box, const Real* points, cons
     return cudaGetLastError();
 }
 
-int harmonics_max_order() { return kHarmMaxOrder; }
+int harmonics_max_order() { return 86; }  // the paired-column kernels to 32, plain kernels above
 
 #define SFMM_INSTANTIATE(Real)                                                                    \
     template cudaError_t launch_p2m<Real>(const int64_t*, const Real*, const Real*, int64_t, int, \

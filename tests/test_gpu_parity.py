@@ -409,7 +409,10 @@ def test_p2m_and_eval_local_bit_exact(oracle, h64, h32, prec):
     ragged boxes incl. empty ones, a charge at the centre (zero argument), orders 1..max."""
     h, dt, pmax = (h64, np.float64, 30) if prec == "f64" else (h32, np.float32, 18)
     rng = np.random.default_rng(409)
-    for p in (1, 2, 5, 9, 16, 17, pmax):
+    big = capi.Handle(capi.F64, 45) if prec == "f64" else None   # orders above 32: the plain kernels
+    for p in (1, 2, 5, 9, 16, 17, pmax) + ((32, 33, 45) if big else ()):
+        if p > pmax:
+            h = big
         counts = np.concatenate([[0, 1, 33], rng.integers(0, 40, 20)])
         box_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
         nb = len(counts)
