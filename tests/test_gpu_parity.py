@@ -582,6 +582,58 @@ def test_precise_mode_removes_the_rounding_floor(oracle, h64, h32):
         h64.set_option("precise", 0)
 
 
+def test_p2m_l2p_at_the_level_shape(oracle, h64):
+    """P2M at the size of BASELINE configs[3] (18 392 source boxes x 32 unit charges, P = 20,
+    written in the rows layout the level kernel gathers) and L2P on 8 192 boxes x 8 points:
+    a sample of boxes / points bit-exact against the oracle, and two size-independent
+    properties on everything: linearity of P2M in the charges, and M_0^0 = total charge."""
+    import torch
+    rng = np.random.default_rng(613)
+    dev = torch.device("cuda", 0)
+    p, nb, per = 20, 38 * 22 * 22, 32
+    S = solid_size(p)
+    t = np.arange(nb)
+    centers = np.stack([t // (22 * 22), (t // 22) % 22, t % 22], 1).astype(np.float64)
+    ch = np.empty((nb * per, 4))
+    ch[:, :3] = np.repeat(centers, per, 0) + rng.random((nb * per, 3)) - 0.5
+    ch[:, 3] = rng.choice([-1.0, 1.0], nb * per)
+    box_ptr = np.arange(0, nb * per + 1, per, dtype=np.int64)
+    d_ptr, d_c = torch.from_numpy(box_ptr).to(dev), torch.from_numpy(centers).to(dev)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def p2m(charges):
+        d_ch = torch.from_numpy(np.ascontiguousarray(charges)).to(dev)
+        d_out = torch.empty((nb, S), dtype=torch.float64, device=dev)
+        h64.p2m(nb, d_ptr.data_ptr(), d_ch.data_ptr(), d_c.data_ptr(), p, capi.LAYOUT_AOS, d_out.data_ptr(), 0, st)
+        torch.cuda.synchronize()
+        return d_out.cpu().numpy()
+
+    m = p2m(ch)
+    for b in rng.integers(0, nb, 40):
+        assert bits_equal(m[b], oracle.p2m_fma(ch[b * per:(b + 1) * per], centers[b], p)), b
+    assert np.array_equal(m[:, 0], ch[:, 3].reshape(nb, per).sum(1))          # R_0^0 = 1, exact sums of +-1
+    doubled = ch.copy()
+    doubled[:, 3] *= 2.0
+    assert np.array_equal(p2m(doubled), 2.0 * m)                               # scaling by 2 is exact
+    # rows layout = pack_rows of the AoS result
+    d_ch = torch.from_numpy(ch).to(dev)
+    d_rows = torch.empty((nb, h64.rows_len(p)), dtype=torch.float64, device=dev)
+    d_ref = torch.empty_like(d_rows)
+    h64.p2m(nb, d_ptr.data_ptr(), d_ch.data_ptr(), d_c.data_ptr(), p, capi.LAYOUT_ROWS, d_rows.data_ptr(), 0, st)
+    h64.pack_rows(nb, p, torch.from_numpy(m).to(dev).data_ptr(), d_ref.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(d_rows, d_ref)
+    # L2P: 8 192 boxes x 8 points; the expansions are the first multipoles (any coefficients do)
+    nt, pts = 8192, 8
+    loc = m[:nt] * 1e-3
+    pb = np.repeat(np.arange(nt, dtype=np.int32), pts)
+    x = centers[pb] + (rng.random((nt * pts, 3)) - 0.5)
+    phi = h64.eval_local_host(pb, x, centers[:nt], p, loc)
+    for i in rng.integers(0, nt * pts, 60):
+        assert phi[i] == oracle.eval_local_fma(p, loc[pb[i]], centers[pb[i]], x[i]), i
+    assert np.all(np.isfinite(phi))
+
+
 # ---- API contracts ---------------------------------------------------------
 
 def test_error_contracts(h64):
