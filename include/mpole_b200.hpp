@@ -474,28 +474,34 @@ std::vector<solid<Real>> read_solids(std::istream& is) {
 
 template <typename Real>
 std::vector<point_charge<Real>> read_charges(std::istream& is) {
-    std::vector<point_charge<Real>> out;
-    std::string line;
-    for (int line_no = 1; std::getline(is, line); ++line_no) {
-        const auto first = line.find_first_not_of(" \t\r");
-        if (first == std::string::npos || line[first] == '#') continue;
-        std::istringstream ls(line);
-        point_charge<Real> c{};
-        std::string rest;
-        if (!(ls >> c.position.x >> c.position.y >> c.position.z >> c.charge))
-            throw std::runtime_error("line " + std::to_string(line_no) + ": expected 'x y z q'");
-        if (ls >> rest)
-            throw std::runtime_error("line " + std::to_string(line_no) + ": trailing content '" + rest + "'");
-        out.push_back(c);
+    std::vector<point_charge<Real>> charges;
+    int line_no = 0;
+    for (std::string line; std::getline(is, line);) {
+        ++line_no;
+        std::istringstream fields(line);
+        std::string first;
+        if (!(fields >> first) || first[0] == '#') continue;  // blank line or comment
+        // four numbers, nothing else
+        Real v[4];
+        std::istringstream again(line);
+        int have = 0;
+        while (have < 4 && (again >> v[have])) ++have;
+        if (have < 4) throw std::runtime_error("line " + std::to_string(line_no) + ": expected 'x y z q'");
+        std::string extra;
+        if (again >> extra)
+            throw std::runtime_error("line " + std::to_string(line_no) + ": trailing content '" + extra + "'");
+        charges.push_back({{v[0], v[1], v[2]}, v[3]});
     }
-    return out;
+    return charges;
 }
 
 template <typename Real>
 void write_charges(std::ostream& os, std::span<const point_charge<Real>> charges) {
     os.precision(std::numeric_limits<Real>::max_digits10);
-    for (const auto& c : charges)
-        os << c.position.x << ' ' << c.position.y << ' ' << c.position.z << ' ' << c.charge << '\n';
+    for (const point_charge<Real>& c : charges) {
+        const Real row[4] = {c.position.x, c.position.y, c.position.z, c.charge};
+        for (int k = 0; k < 4; ++k) os << row[k] << (k == 3 ? '\n' : ' ');
+    }
 }
 
 }  // namespace mpole_b200
