@@ -463,6 +463,7 @@ def test_p2m_layouts_feed_the_translation_path(oracle, h64):
     want = np.stack([oracle.p2m_fma(ch[b * per:(b + 1) * per], centers[b], p) for b in range(nb)])
     assert bits_equal(d_aos.cpu().numpy(), want)
     assert bits_equal(d_soa.cpu().numpy()[:, :nb].T, want)
+    assert torch.all(d_soa[:, nb:] == 0)                 # padding columns untouched
     d_rows_ref = torch.empty_like(d_rows)
     h64.pack_rows(nb, p, d_aos.data_ptr(), d_rows_ref.data_ptr(), st)
     torch.cuda.synchronize()
@@ -475,10 +476,12 @@ def test_p2m_layouts_feed_the_translation_path(oracle, h64):
     lc = centers + sh
     x = lc + (rng.random((nb, 3)) - 0.5) * 0.5
     d_lc, d_x = torch.from_numpy(lc).to(dev), torch.from_numpy(x).to(dev)
-    d_phi = torch.empty(nb, dtype=torch.float64, device=dev)
+    d_phi_all = torch.full((nb + 64,), 9.0, dtype=torch.float64, device=dev)   # guard band behind the output
+    d_phi = d_phi_all[:nb]
     h64.eval_local(nb, None, d_x.data_ptr(), d_lc.data_ptr(), nb, p, capi.LAYOUT_SOA, d_loc.data_ptr(), stride,
                    d_phi.data_ptr(), st)
     torch.cuda.synchronize()
+    assert torch.all(d_phi_all[nb:] == 9.0)
     loc = oracle.translate("m2l", p, p, want, sh)[1]
     phi = np.array([oracle.eval_local_fma(p, loc[b], lc[b], x[b]) for b in range(nb)])
     assert bits_equal(d_phi.cpu().numpy(), phi)
