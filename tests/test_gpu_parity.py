@@ -623,7 +623,8 @@ def test_p2m_l2p_at_the_level_shape(oracle, h64):
     d_rows = torch.empty((nb, h64.rows_len(p)), dtype=torch.float64, device=dev)
     d_ref = torch.empty_like(d_rows)
     h64.p2m(nb, d_ptr.data_ptr(), d_ch.data_ptr(), d_c.data_ptr(), p, capi.LAYOUT_ROWS, d_rows.data_ptr(), 0, st)
-    h64.pack_rows(nb, p, torch.from_numpy(m).to(dev).data_ptr(), d_ref.data_ptr(), st)
+    d_m = torch.from_numpy(m).to(dev)
+    h64.pack_rows(nb, p, d_m.data_ptr(), d_ref.data_ptr(), st)
     torch.cuda.synchronize()
     assert torch.equal(d_rows, d_ref)
     # L2P: 8 192 boxes x 8 points; the expansions are the first multipoles (any coefficients do)
