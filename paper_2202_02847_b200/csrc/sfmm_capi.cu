@@ -657,11 +657,9 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
     // declared before the guard below: the guard drains the streams first, then the buffers go
     DevBuf d_src_aos(sc), d_src(sc), d_flags(sc);
     std::vector<std::unique_ptr<Slab>> slabs;
-    cudaEvent_t ev_src = nullptr;
     struct Drain {
         cudaStream_t a, b;
         std::vector<std::unique_ptr<Slab>>* slabs;
-        cudaEvent_t* ev;
         ~Drain() {
             cudaStreamSynchronize(a);
             cudaStreamSynchronize(b);
@@ -676,11 +674,9 @@ sfmm_status level_host_impl(sfmm_handle* h, int64_t n_targets, const int64_t* tg
                 if (p.d_angle_index) cudaFreeAsync(p.d_angle_index, a);
                 if (p.d_grp_target) cudaFreeAsync(p.d_grp_target, a);
             }
-            if (*ev) cudaEventDestroy(*ev);
         }
-    } drain{sc, sx, &slabs, &ev_src};
+    } drain{sc, sx, &slabs};
 
-    CU(cudaEventCreateWithFlags(&ev_src, cudaEventDisableTiming));
     CU(d_src_aos.alloc(es * si * n_sources));
     CU(d_src.alloc(es * srows * n_sources));
     CU(d_flags.alloc(sizeof(int) * 2 * K));
