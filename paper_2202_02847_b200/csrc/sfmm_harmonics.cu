@@ -216,7 +216,11 @@ p2m_kernel(const int64_t* __restrict__ box_ptr, const Real* __restrict__ charges
 // dynamic shared memory: denom [P][P+1] | per warp and sub-group: locals [P(P+1)], terms
 // [P(P+1)/2], rows [P]
 extern __shared__ __align__(16) unsigned char harm_smem[];
-template <typename Real>
+// STAGE: the local expansion of the current box is copied to shared memory (SoA / rows
+// layouts, whose global accesses are strided); without it (AoS layout) the lanes read it
+// straight from global memory through L1 — the 3.4 KB of a box are reused by all its points —
+// and the shared memory saved lets 2.6x as many warps run per SM.
+template <typename Real, bool STAGE>
 __global__ void __launch_bounds__(128)
 eval_local_kernel(const int32_t* __restrict__ point_box, const Real* __restrict__ points,
                   const Real* __restrict__ centers, int64_t n_points, int64_t n_boxes, int order,
@@ -227,10 +231,10 @@ eval_local_kernel(const int32_t* __restrict__ point_box, const Real* __restrict_
     const int half = (order + 1) >> 1, per_warp = 32 / half;
     const int sub = lane / half, l = lane - sub * half;
     const bool lane_on = sub < per_warp;
-    const size_t per_sub = (size_t)S + (size_t)S / 2 + order;  // locals, terms (triangle), rows
+    const size_t per_sub = (STAGE ? (size_t)S : 0) + (size_t)S / 2 + order;  // locals, terms (triangle), rows
     Real* denom = reinterpret_cast<Real*>(harm_smem);
     Real* my_loc = denom + order * LD + ((size_t)w * per_warp + (lane_on ? sub : 0)) * per_sub;
-    Real* my_terms = my_loc + S;
+    Real* my_terms = my_loc + (STAGE ? S : 0);
     Real* my_rows = my_terms + S / 2;
     if (threadIdx.x <= kHarmMaxOrder) inv2n[threadIdx.x] = threadIdx.x ? Real(1) / Real(2 * (int)threadIdx.x) : Real(0);
     for (int i = threadIdx.x; i < order * LD; i += blockDim.x) {
@@ -256,7 +260,7 @@ eval_local_kernel(const int32_t* __restrict__ point_box, const Real* __restrict_
             on = false;
             b = -1;
         }
-        if (on && b != cached) {  // the lanes of a sub-group agree
+        if (STAGE && on && b != cached) {  // the lanes of a sub-group agree
             if (layout == LAYOUT_AOS) {
                 for (int c = l; c < S; c += half) my_loc[c] = locals[b * S + c];
             } else {
@@ -276,7 +280,8 @@ eval_local_kernel(const int32_t* __restrict__ point_box, const Real* __restrict_
                 const int m = second ? mB : mA, k = second ? s - cA : s, n = m + k;
                 Real vre, vim;
                 st.slot(n, m, k, s == cA, denom[n * LD + m], vre, vim);
-                const Real lre = my_loc[n * (n + 1) + 2 * m], lim = my_loc[n * (n + 1) + 2 * m + 1];
+                const Real* lp = STAGE ? my_loc : locals + b * S;
+                const Real lre = lp[n * (n + 1) + 2 * m], lim = lp[n * (n + 1) + 2 * m + 1];
                 // column 0 keeps the two factors apart: total = fma(L_n^0, R_n^0, total)
                 my_terms[n * (n + 1) / 2 + m] = m == 0 ? vre : fma_(lre, vre, lim * vim);
             }
@@ -296,7 +301,7 @@ eval_local_kernel(const int32_t* __restrict__ point_box, const Real* __restrict_
         if (on && l == 0) {
             Real total_sum = Real(0);
             for (int n = 0; n < order; ++n) {
-                total_sum = fma_(my_loc[n * (n + 1)], my_terms[n * (n + 1) / 2], total_sum);
+                total_sum = fma_((STAGE ? my_loc : locals + b * S)[n * (n + 1)], my_terms[n * (n + 1) / 2], total_sum);
                 const Real r = my_rows[n];
                 total_sum = total_sum + (r + r);
             }
@@ -445,16 +450,18 @@ cudaError_t launch_eval_local(const int32_t* point_box, const Real* points, cons
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int per_warp = 32 / ((order + 1) / 2);
+    const bool stage = layout != LAYOUT_AOS;
     const size_t smem = sizeof(Real) * ((size_t)order * (order + 1) +
-                                        4 * per_warp * ((size_t)order * (order + 1) * 3 / 2 + order));
-    cudaError_t e = cudaFuncSetAttribute(eval_local_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                        4 * per_warp * ((size_t)order * (order + 1) * (stage ? 3 : 1) / 2 + order));
+    auto kern = stage ? eval_local_kernel<Real, true> : eval_local_kernel<Real, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_local_kernel<Real>, 128, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)std::min<int64_t>((n_points + 3) / 4, (int64_t)sms * std::max(per_sm, 1));
-    eval_local_kernel<Real><<<grid, 128, smem, stream>>>(point_box, points, centers, n_points, n_boxes, order,
-                                                      layout, locals, stride, out);
+    kern<<<grid, 128, smem, stream>>>(point_box, points, centers, n_points, n_boxes, order, layout, locals, stride,
+                                      out);
     return cudaGetLastError();
 }
 
