@@ -156,7 +156,7 @@ __device__ void swap_half_task(const HalfTaskCtx<Real>& c, int n, int cls) {
 // state between the two swaps and every deviation of (cos, sin)(m beta) from a point of the unit
 // circle. Carrying that state in double-double, from cos beta = z / |r| itself through the
 // recurrence, both products and the rotation, and rounding once at the end, removes it
-// (1e-14 at P = 20, 2e-14 at P = 24: tools/accuracy_report.py). Rounding the state in the
+// (1e-14 at P = 20, 2e-14 at P = 24: tests/tools/accuracy_report.py). Rounding the state in the
 // middle, or keeping the double tables, gives most of the loss back. Everything else (forward
 // pass, z-step, alpha rotations) stays in double as in the reference.
 struct dd {

@@ -13,12 +13,12 @@ solid, tests/test_helpers.hpp:41-55), maximum over the batch. L2L has no naive k
 rows compare against the two reference builds and report the there-and-back error."""
 import sys
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent.parent))
 import numpy as np
 from paper_2202_02847_b200 import capi, workloads
 from tests.oracle_lib import Reference, Oracle, normalized_error
 
-ROOT = Path(__file__).resolve().parent.parent
+ROOT = Path(__file__).resolve().parent.parent.parent
 N = 256
 fma, nofma = Reference.try_load("fma"), Reference.try_load("nofma")
 if fma is None or nofma is None:
@@ -51,7 +51,7 @@ for p in (8, 12, 16, 20, 24, 30):
                      normalized_error(back, gpu), bool(np.array_equal(g2, f2)), normalized_error(back_precise, gpu)))
 h.close()
 
-out = ["# Accuracy report, round 2 (tools/accuracy_report.py, one B200)", "",
+out = ["# Accuracy report, round 2 (tests/tools/accuracy_report.py, one B200)", "",
        f"{N} translations per order, FP64, `normalized_error` (max over the batch). The parity target is the",
        "reference's FMA build; the no-FMA column is the reference's default CMake arithmetic; `naive` is",
        "the reference's own O(P^4) accuracy oracle.", "",

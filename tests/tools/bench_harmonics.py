@@ -6,7 +6,7 @@ steps), roofline (slower of flops at the FP64 peak and bytes at the HBM bandwidt
 end through the host entry points, and the reference's CPU functions (oracle/_ref,
 mpole::p2m / mpole::eval_local, one thread) on a bounded sample.
 
-    python tools/bench_harmonics.py [--steps K] [--warmup W] > gpurun_out/harmonics.jsonl
+    python tests/tools/bench_harmonics.py [--steps K] [--warmup W] > gpurun_out/harmonics.jsonl
 """
 import argparse
 import json
@@ -16,7 +16,7 @@ from pathlib import Path
 
 import numpy as np
 
-ROOT = Path(__file__).resolve().parent.parent
+ROOT = Path(__file__).resolve().parent.parent.parent
 sys.path.insert(0, str(ROOT))
 from paper_2202_02847_b200 import capi  # noqa: E402
 

@@ -1,7 +1,7 @@
 """Quick GPU parity probe: CUDA library vs the CPU oracle on random requests."""
 import sys, time
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent.parent))
 import numpy as np
 from paper_2202_02847_b200 import capi
 from tests.oracle_lib import Oracle, normalized_error
@@ -30,6 +30,14 @@ for dt, prec, pmax in ((np.float64, capi.F64, 30 if variant != 2 else 20), (np.f
         assert st == 0
         got = h.translate_host(kind, pin, pout, x, sh)
         same = np.array_equal(got, want, equal_nan=True)
+        if not same and not np.isfinite(want).all():
+            # single precision overflows at high order and short shifts ((n+k)! / r^(n+k+1)); the
+            # reference's result is not finite there and the comparison is restricted to the
+            # solids that are (the kernels skip multiplications by exact zeros, so the two
+            # sides need not agree on which non-finite value a poisoned solid carries)
+            fin = np.isfinite(want).all(axis=1)
+            same = np.array_equal(got[fin], want[fin])
+            print(f"  ({(~fin).sum()} of {n} solids are not finite in the reference: compared the rest)")
         err = 0.0 if same else normalized_error(got, want)
         if not same: bad += 1
         print(f"{dt.__name__} kind={kind} p_in={pin:2d} p_out={pout:2d} n={n:3d} bit-exact={same} err={err:.2e}", flush=True)

@@ -1,7 +1,7 @@
 """Parity of the small-order kernel (variant 4) against the CPU oracle, all orders <= 8."""
 import sys
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent.parent))
 import numpy as np
 from paper_2202_02847_b200 import capi
 from tests.oracle_lib import Oracle

@@ -3,7 +3,7 @@ levels, for hang and crash detection; every result is checked for finiteness and
 sample, bit for bit against the CPU oracle."""
 import sys, time
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent.parent))
 import numpy as np
 from paper_2202_02847_b200 import capi
 from tests.helpers import random_solids, random_shifts
