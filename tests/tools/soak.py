@@ -10,7 +10,8 @@ from tests.helpers import random_solids, random_shifts
 from tests.oracle_lib import Oracle
 
 orc = Oracle()
-rng = np.random.default_rng(5)
+import os
+rng = np.random.default_rng(int(os.environ.get("SOAK_SEED", "5")))
 h64 = capi.Handle(capi.F64, 30); h32 = capi.Handle(capi.F32, 12)
 t0 = time.time(); n_calls = 0
 names = {capi.M2L: "m2l", capi.M2M: "m2m", capi.L2L: "l2l"}
