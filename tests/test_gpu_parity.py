@@ -638,6 +638,37 @@ def test_p2m_l2p_at_the_level_shape(oracle, h64):
     assert np.all(np.isfinite(phi))
 
 
+def test_level_repeats_bit_identically(h64):
+    """The tiled kernel orders its phases with shared-memory flags (row_done, row_a_done) and an
+    mbarrier instead of CTA barriers: a race would show as run-to-run differences. A level of
+    2 048 targets, twelve repetitions in each accumulation mode, identical bits throughout."""
+    import torch
+    dev = torch.device("cuda", 0)
+    p = 20
+    src, tp, si, shf = workloads.config3(5, (16, 16, 8), p)
+    ns, nt, S = len(src), len(tp) - 1, solid_size(p)
+    plan = h64.plan(tp, si, shf, ns)
+    d_aos = torch.from_numpy(src).to(dev)
+    d_rows = torch.empty((ns, h64.rows_len(p)), dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    h64.pack_rows(ns, p, d_aos.data_ptr(), d_rows.data_ptr(), st)
+    ostride = (nt + 31) // 32 * 32
+    ref = None
+    try:
+        for mode in (0, 1):
+            h64.set_option("accumulate_plain", mode)
+            for r in range(12):
+                d_out = torch.full((S, ostride), float(r), dtype=torch.float64, device=dev)
+                plan.accumulate_rows(p, p, d_rows.data_ptr(), d_out.data_ptr(), ostride, st)
+                torch.cuda.synchronize()
+                got = d_out[:, :nt].clone()
+                ref = got if ref is None else ref
+                assert torch.equal(got, ref), (mode, r)
+    finally:
+        h64.set_option("accumulate_plain", 0)
+        plan.close()
+
+
 # ---- API contracts ---------------------------------------------------------
 
 def test_error_contracts(h64):
