@@ -451,7 +451,7 @@ struct TiledLayout {
     // counters of the backward swap pass, launch constants of the row function
     __host__ __device__ size_t smem_bytes() const {
         return sizeof(Real) * (buf_elems() + tab_len) + 32 + 2 * sizeof(int) * ((PMAX + 3) / 4 * 4) +
-               128;  // RowConst
+               128 + 8 * PMAX;  // RowConst, row_bar (phase A by bulk copies)
     }
 };
 
@@ -656,7 +656,11 @@ template <int TL, int ACC, bool ROWS, int CHA>
 __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int gen, int flags) {
     constexpr int L = 32 * TL;
     // CHA: elements per batch of phase-A loads (2; 4 for streamed SoA inputs at the orders where
-    // it was measured to pay, launch_translate_tiled)
+    // it was measured to pay, launch_translate_tiled). CHA == 0: phase A of a streamed (SoA) group
+    // by bulk copies: a coefficient plane of the group is L contiguous values that land in one
+    // row of the triangle, so the 2n+1 planes of row n are requested at once (cp.async.bulk, one
+    // per lane, completion on the row's mbarrier) and rotated in place when they are there: one
+    // memory latency per row instead of one per load batch, no registers in flight.
     const int lane = threadIdx.x & 31;
     const int misc_off = flags >> ROWS_MISC_SHIFT;  // bytes: {mbarrier, counters, row_done, RowConst}
     int* counters = reinterpret_cast<int*>(smem_raw + misc_off + 8);
@@ -667,6 +671,11 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
     const int i1 = min(1, p_rot - 1);  // row of cos/sin(alpha) in the tables
     Real* buf = reinterpret_cast<Real*>(smem_raw) + e.buf_off + lane;
     const bool do_d = flags & ROWS_D, do_a = flags & ROWS_A;
+    constexpr bool BULK = CHA == 0;
+    constexpr int CB = BULK ? 2 : CHA;  // register batches (BULK: only the last, partial group)
+    uint64_t* row_bar = reinterpret_cast<uint64_t*>(smem_raw + misc_off + 32 + ROW_DONE_BYTES + 128);
+    const bool bulk_ok = BULK && !ROWS && do_a && (g_a + 1) * (int64_t)L <= e.n_total &&
+                         (e.in_stride * sizeof(Real)) % 16 == 0 && (reinterpret_cast<uintptr_t>(e.in) & 15) == 0;
     const Real* geo_d = e.geo_base + ((flags & ROWS_PARITY_D) ? e.geo_stride : 0);
     const Real* geo_a = e.geo_base + ((flags & ROWS_PARITY_A) ? e.geo_stride : 0);
     const GeoView<TL> gvd((do_d ? geo_d : geo_a) + lane, p_rot);
@@ -721,12 +730,12 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
         Real* rowp = buf + n * n * L;
 
         // ---- A, first part: the loads of the first batch are in flight during phase D
-        Real are[CHA][TL], aim[CHA][TL];
+        Real are[CB][TL], aim[CB][TL];
         const int64_t row_off = ROWS ? rows_off(n) : (int64_t)aos_re(n, 0) * e.in_stride;
         auto issue = [&](int m0) {
             if constexpr (ROWS) {
 #pragma unroll
-                for (int j = 0; j < CHA / 2; ++j) {
+                for (int j = 0; j < CB / 2; ++j) {
                     const int64_t off = row_off + 4 * min((m0 >> 1) + j, n >> 1);
 #pragma unroll
                     for (int t = 0; t < TL; ++t) {
@@ -740,7 +749,7 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
                 }
             } else {
 #pragma unroll
-                for (int u = 0; u < CHA; ++u) {
+                for (int u = 0; u < CB; ++u) {
                     const int64_t off = row_off + (int64_t)(2 * min(m0 + u, n)) * e.in_stride;
 #pragma unroll
                     for (int t = 0; t < TL; ++t) {
@@ -754,7 +763,7 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
         if (row_a) {
 #pragma unroll
             for (int t = 0; t < TL; ++t) aq[t] = acta[t] ? gva.qa[n * L + 32 * t] : Real(0);
-            issue(0);
+            if (!bulk_ok) issue(0);
         }
 
         // ---- D
@@ -858,9 +867,43 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
             c[t] = Real(1);
             s[t] = Real(0);
         }
+        if (bulk_ok) {
+            // every lane has finished phase D of this row; the planes of the next group replace it
+            __syncwarp();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (lane == 0) mbar_expect_tx(&row_bar[n], (uint32_t)((2 * n + 1) * L * sizeof(Real)));
+            __syncwarp();
+            Real* row_base = reinterpret_cast<Real*>(smem_raw) + e.buf_off + n * n * L;
+            for (int j = lane; j <= 2 * n; j += 32) {
+                // triangle position j of the row: re(m) at 2m, im(m) at 2m-1; AoS index of the plane
+                const int cq = n * (n + 1) + ((j & 1) ? j + 2 : j);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                        "r"(smem_u32(row_base + j * L)),
+                    "l"(e.in + (int64_t)cq * e.in_stride + g_a * L), "r"((uint32_t)(L * sizeof(Real))),
+                    "r"(smem_u32(&row_bar[n]))
+                    : "memory");
+            }
+            mbar_wait(&row_bar[n], (uint32_t)(gen & 1));
+            for (int m = 0; m <= n; ++m) {
+#pragma unroll
+                for (int t = 0; t < TL; ++t) {
+                    const Real xr = rowp[(2 * m) * L + 32 * t];
+                    const Real xi = m ? rowp[(2 * m - 1) * L + 32 * t] : Real(0);
+                    const Real nr = aq[t] * fma_(xr, c[t], -(xi * s[t]));
+                    const Real ni = aq[t] * fma_(xr, s[t], xi * c[t]);
+                    rowp[(2 * m) * L + 32 * t] = nr;
+                    if (m) rowp[(2 * m - 1) * L + 32 * t] = ni;
+                    const Real nc = fma_(c[t], ac1[t], -(s[t] * as1[t]));
+                    const Real ns = fma_(s[t], ac1[t], c[t] * as1[t]);
+                    c[t] = nc;
+                    s[t] = ns;
+                }
+            }
+        } else
         for (int m0 = 0;;) {
 #pragma unroll
-            for (int u = 0; u < CHA; ++u) {
+            for (int u = 0; u < CB; ++u) {
                 const int m = m0 + u;
                 if (m > n) break;
 #pragma unroll
@@ -878,7 +921,7 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
                     s[t] = ns;
                 }
             }
-            m0 += CHA;
+            m0 += CB;
             if (m0 > n) break;
             issue(m0);
         }
@@ -929,6 +972,9 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
     if (threadIdx.x < 6) counters[threadIdx.x] = 0;
     int* row_a_done = row_done + ROW_DONE_INTS;        // [PMAX] trip + 1 of the last finished phase A per row
     if (threadIdx.x < PMAX) row_done[threadIdx.x] = row_a_done[threadIdx.x] = 0;
+    if (CHA == 0 && threadIdx.x < PMAX)
+        mbar_init(reinterpret_cast<uint64_t*>(smem_raw + (sizeof(Real) * (lay.tab_len + lay.buf_elems())) + 32 +
+                                              ROW_DONE_BYTES + 128) + threadIdx.x, 1);
 
     // per-phase cycle counters of CTA 0 (tuning aid, tools/perf_probe.py PHASES=1): compiled in
     // only with -DSFMM_PHASE_CLOCKS, because the running time stamp costs every warp a
@@ -1219,9 +1265,14 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     // streamed SoA inputs: four-element load batches in phase A where 12 warps run one group per
     // SM (measured: P = 16 +8 %; P = 12 -3 %, 14 -8 %, 20 -3 % with two CTAs per SM or a full SM)
     const bool wide = sizeof(Real) == 8 && p_rot >= 15 && p_rot <= 18;
+    // phase A by bulk copies (measured on / off, batched M2L, 400 000 translations, f64: P = 10
+    // -1.4 %, 12 +2.6 %, 14 +0.8 %, 16 +2.2 %, 18 +3.0 %, 20 +2.7 %)
+    const bool bulk_a = getenv("SFMM_TILED_BULK_A") ? atoi(getenv("SFMM_TILED_BULK_A")) != 0
+                                                     : p_rot >= 12;  // f32: P = 12 +1.0 %, 18 +1.7 %
     if (mode == ACC_NONE)
         kern = rows ? translate_tiled_kernel<TL, ACC_NONE, true>
-                    : (wide ? translate_tiled_kernel<TL, ACC_NONE, false, 4> : translate_tiled_kernel<TL, ACC_NONE, false>);
+                    : (bulk_a ? translate_tiled_kernel<TL, ACC_NONE, false, 0>
+                              : (wide ? translate_tiled_kernel<TL, ACC_NONE, false, 4> : translate_tiled_kernel<TL, ACC_NONE, false>));
     else if (mode == ACC_PLAIN) kern = rows ? translate_tiled_kernel<TL, ACC_PLAIN, true> : translate_tiled_kernel<TL, ACC_PLAIN, false>;
     else kern = rows ? translate_tiled_kernel<TL, ACC_L2ADD, true> : translate_tiled_kernel<TL, ACC_L2ADD, false>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
