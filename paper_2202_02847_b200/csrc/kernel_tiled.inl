@@ -1265,10 +1265,11 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     // streamed SoA inputs: four-element load batches in phase A where 12 warps run one group per
     // SM (measured: P = 16 +8 %; P = 12 -3 %, 14 -8 %, 20 -3 % with two CTAs per SM or a full SM)
     const bool wide = sizeof(Real) == 8 && p_rot >= 15 && p_rot <= 18;
-    // phase A by bulk copies (measured on / off, batched M2L, 400 000 translations, f64: P = 10
-    // -1.4 %, 12 +2.6 %, 14 +0.8 %, 16 +2.2 %, 18 +3.0 %, 20 +2.7 %)
-    const bool bulk_a = getenv("SFMM_TILED_BULK_A") ? atoi(getenv("SFMM_TILED_BULK_A")) != 0
-                                                     : p_rot >= 12;  // f32: P = 12 +1.0 %, 18 +1.7 %
+    // phase A by bulk copies: off by default. kernel-only timings without an L2 flush gain (batched
+    // M2L, 400 000 translations, f64: P = 12 +2.6 %, 16 +2.2 %, 18 +3.0 %, 20 +2.7 %, 10 -1.4 %), the
+    // bench lines (inputs from HBM, L2 flushed between steps) do not (P = 14 -2.8 %, 16 +1.8 %, 18
+    // -0.7 %, 20 +1.0 %, configs[1] -0.5 %): SFMM_TILED_BULK_A=1 selects it
+    const bool bulk_a = getenv("SFMM_TILED_BULK_A") ? atoi(getenv("SFMM_TILED_BULK_A")) != 0 : false;
     if (mode == ACC_NONE)
         kern = rows ? translate_tiled_kernel<TL, ACC_NONE, true>
                     : (bulk_a ? translate_tiled_kernel<TL, ACC_NONE, false, 0>
