@@ -884,22 +884,7 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
                     "r"(smem_u32(&row_bar[n]))
                     : "memory");
             }
-            mbar_wait(&row_bar[n], (uint32_t)(gen & 1));
-            for (int m = 0; m <= n; ++m) {
-#pragma unroll
-                for (int t = 0; t < TL; ++t) {
-                    const Real xr = rowp[(2 * m) * L + 32 * t];
-                    const Real xi = m ? rowp[(2 * m - 1) * L + 32 * t] : Real(0);
-                    const Real nr = aq[t] * fma_(xr, c[t], -(xi * s[t]));
-                    const Real ni = aq[t] * fma_(xr, s[t], xi * c[t]);
-                    rowp[(2 * m) * L + 32 * t] = nr;
-                    if (m) rowp[(2 * m - 1) * L + 32 * t] = ni;
-                    const Real nc = fma_(c[t], ac1[t], -(s[t] * as1[t]));
-                    const Real ns = fma_(s[t], ac1[t], c[t] * as1[t]);
-                    c[t] = nc;
-                    s[t] = ns;
-                }
-            }
+            continue;  // rotated by a later task of this phase, when the planes have landed
         } else
         for (int m0 = 0;;) {
 #pragma unroll
@@ -930,6 +915,42 @@ __device__ __forceinline__ void elementwise_rows(int64_t g_d, int64_t g_a, int g
         if (lane == 0) {
             __threadfence_block();
             *reinterpret_cast<volatile int*>(&row_a_done[n]) = gen + 1;
+        }
+    }
+    // bulk form of phase A, second half: every row task has been taken (and its copies are issued
+    // or will be by the warp that holds it); rotate the rows, longest first, as their planes land
+    if (bulk_ok) {
+        for (int task = fetch_task(&counters[5], lane); task < e.p_in; task = fetch_task(&counters[5], lane)) {
+            const int n = e.p_in - 1 - task;
+            Real* rowp = buf + n * n * L;
+            Real c[TL], s[TL], aq[TL];
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                aq[t] = acta[t] ? gva.qa[n * L + 32 * t] : Real(0);
+                c[t] = Real(1);
+                s[t] = Real(0);
+            }
+            mbar_wait(&row_bar[n], (uint32_t)(gen & 1));
+            for (int m = 0; m <= n; ++m) {
+#pragma unroll
+                for (int t = 0; t < TL; ++t) {
+                    const Real xr = rowp[(2 * m) * L + 32 * t];
+                    const Real xi = m ? rowp[(2 * m - 1) * L + 32 * t] : Real(0);
+                    const Real nr = aq[t] * fma_(xr, c[t], -(xi * s[t]));
+                    const Real ni = aq[t] * fma_(xr, s[t], xi * c[t]);
+                    rowp[(2 * m) * L + 32 * t] = nr;
+                    if (m) rowp[(2 * m - 1) * L + 32 * t] = ni;
+                    const Real nc = fma_(c[t], ac1[t], -(s[t] * as1[t]));
+                    const Real ns = fma_(s[t], ac1[t], c[t] * as1[t]);
+                    c[t] = nc;
+                    s[t] = ns;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                *reinterpret_cast<volatile int*>(&row_a_done[n]) = gen + 1;
+            }
         }
     }
 }
@@ -1113,7 +1134,7 @@ translate_tiled_kernel(TranslateArgs<Real> a, TiledTables tt, int64_t n_groups, 
         }
         __syncthreads();
         SFMM_PHASE_MARK(2)
-        if (threadIdx.x == 0) counters[0] = counters[2] = counters[3] = counters[4] = 0;
+        if (threadIdx.x == 0) counters[0] = counters[2] = counters[3] = counters[4] = counters[5] = 0;
         if (two_sides) {  // stage the backward-side stream while the z-step runs
             if (threadIdx.x == 0) bulk_load(tab, tt.stream[side_bwd], tt.bytes[1], mbar);
             tab_pending = true;
@@ -1265,11 +1286,10 @@ cudaError_t launch_translate_tiled(const DeviceTables<Real>& t, const TranslateA
     // streamed SoA inputs: four-element load batches in phase A where 12 warps run one group per
     // SM (measured: P = 16 +8 %; P = 12 -3 %, 14 -8 %, 20 -3 % with two CTAs per SM or a full SM)
     const bool wide = sizeof(Real) == 8 && p_rot >= 15 && p_rot <= 18;
-    // phase A by bulk copies: off by default. kernel-only timings without an L2 flush gain (batched
-    // M2L, 400 000 translations, f64: P = 12 +2.6 %, 16 +2.2 %, 18 +3.0 %, 20 +2.7 %, 10 -1.4 %), the
-    // bench lines (inputs from HBM, L2 flushed between steps) do not (P = 14 -2.8 %, 16 +1.8 %, 18
-    // -0.7 %, 20 +1.0 %, configs[1] -0.5 %): SFMM_TILED_BULK_A=1 selects it
-    const bool bulk_a = getenv("SFMM_TILED_BULK_A") ? atoi(getenv("SFMM_TILED_BULK_A")) != 0 : false;
+    // phase A by bulk copies, the planes requested by the warp that finishes phase D of a row and
+    // rotated by a later task (bench lines, L2 flushed, on / off: configs[1] +0.7 %, sweep P = 14
+    // +1.5 %, 16 +2.7 %, 20 +6.1 %); SFMM_TILED_BULK_A=0 / 1 overrides
+    const bool bulk_a = getenv("SFMM_TILED_BULK_A") ? atoi(getenv("SFMM_TILED_BULK_A")) != 0 : p_rot >= 12;
     if (mode == ACC_NONE)
         kern = rows ? translate_tiled_kernel<TL, ACC_NONE, true>
                     : (bulk_a ? translate_tiled_kernel<TL, ACC_NONE, false, 0>
