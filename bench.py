@@ -84,6 +84,12 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.15)
         self.proc.terminate()
+        try:
+            # nvidia-smi must be GONE before anything else is timed: its teardown holds a
+            # driver-wide lock for ~100 ms, which showed up as one 96 ms end-to-end step
+            self.proc.wait(timeout=10)
+        except Exception:
+            pass
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ts, line in self.rows:
@@ -535,10 +541,13 @@ def main():
             step_e2e()
         barrier()
         t0 = time.perf_counter()
+        marks = []
         for _ in range(e2e_steps):
             step_e2e()
+            marks.append(time.perf_counter())
         barrier()
         my_e2e = (time.perf_counter() - t0) / e2e_steps
+        log("e2e step times (ms):", " ".join(f"{(b - a) * 1e3:.2f}" for a, b in zip([t0] + marks[:-1], marks)))
         e2e_units_total = total_units if case.level else len(out_host) * world
 
     if world > 1:
